@@ -1,0 +1,167 @@
+/* pgmres.h — C ABI of the B200-native deflated PGMRES library (libpgmres.so).
+ *
+ * Drop-in boundary for the reference's linear-solve path.  Each entry point
+ * replaces one reference interface (file:line into /root/reference/proj):
+ *
+ *   pgm_solve ................ deflated_gmres(A, b, x, cfg, Deflator&, Executor&)
+ *                              include/dgmres/deflation.hpp:97-98, and
+ *                              gmres_restarted(opA=spmv, opM=nullptr, ...)
+ *                              include/dgmres/gmres.hpp:110-113 (deflator NULL)
+ *   pgm_context_create ....... Executor(Partition, deterministic)  parallel.hpp:86-91
+ *                              + partition_rows                     parallel.hpp:43
+ *   pgm_matrix_upload ........ CsrMatrix hand-off                   sparse.hpp:17-24
+ *   pgm_matrix_update_values . assemble_jacobian value rewrite      assembly.cpp:253,288
+ *   pgm_spmv ................. Executor::spmv                       parallel.hpp:93
+ *   pgm_deflator_* ........... class Deflator                       deflation.hpp:35-89
+ *   pgm_report_* ............. GmresReport / write_csv              gmres.hpp:31-44
+ *
+ * Conventions: plain pointers and sizes; every function returns a pgm_status
+ * (0 = OK).  The message of the last failure is pgm_last_error(ctx).  Host
+ * pointers unless the PGM_DEVICE_PTRS flag says the arrays are CUDA device
+ * memory on the context's device.  All arithmetic is fp64; indices are
+ * uint32 like the reference's index_t (mesh.hpp:8).
+ */
+#ifndef PGMRES_H_
+#define PGMRES_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PGM_OK = 0,
+  PGM_EINVAL = 1,     /* std::invalid_argument in the reference            */
+  PGM_ENONFINITE = 2, /* gmres.cpp:151-153,165-169,195-198 runtime_error   */
+  PGM_ESINGULAR = 3,  /* gmres.cpp:97-99 singular projection               */
+  PGM_ECUDA = 4,
+  PGM_ENCCL = 5,
+  PGM_ENOMEM = 6,
+  PGM_ESTATE = 7
+} pgm_status;
+
+enum { PGM_DEVICE_PTRS = 1 };
+
+typedef struct pgm_context pgm_context;
+typedef struct pgm_matrix pgm_matrix;
+typedef struct pgm_deflator pgm_deflator;
+
+/* One rank of a z-slab row-block partition (parallel.cpp:50-71). */
+typedef struct {
+  int32_t device;         /* CUDA ordinal this rank drives                   */
+  int32_t rank, world;    /* world = 1: single GPU                           */
+  const void* nccl_id;    /* 128-byte ncclUniqueId from rank 0 (world > 1)   */
+  uint32_t n_axis;        /* node planes; plane = n_axis^2 rows (0: n/world   */
+                          /* contiguous split without mesh structure)        */
+  uint32_t n_global;      /* total rows                                      */
+  int32_t deterministic;  /* reserved: reduction order is always fixed       */
+} pgm_context_config;
+
+typedef struct {
+  uint32_t row_begin, row_end;  /* owned rows [begin, end)                   */
+  uint32_t halo_lo, halo_hi;    /* halo rows read below / above              */
+} pgm_partition;
+
+typedef struct {
+  uint32_t n;               /* rows in this view (owned rows of this rank)   */
+  uint64_t nnz;
+  const uint32_t* row_ptr;  /* n+1 offsets starting at 0                     */
+  const uint32_t* col_idx;  /* GLOBAL column ids, ascending within a row     */
+  const double* values;
+} pgm_csr_view;
+
+typedef struct { /* GmresConfig, gmres.hpp:17-23 */
+  uint32_t m;
+  uint32_t max_restarts;
+  double rel_tol;
+  int32_t fixed_iterations;
+  double breakdown_scale;
+} pgm_gmres_config;
+
+typedef struct { /* DeflationConfig, deflation.hpp:15-22 */
+  uint32_t r_max;
+  uint32_t drop;
+  double accept_tol;
+  uint32_t inv_power_maxit;
+  double inv_power_tol;
+  uint32_t power_maxit;
+} pgm_deflation_config;
+
+typedef struct { /* GmresReport, gmres.hpp:31-44 (arrays owned; pgm_report_free) */
+  double beta0;
+  uint32_t restarts;
+  uint64_t total_inner;
+  int32_t converged;
+  int32_t breakdown;
+  double final_relative;
+  uint32_t n_inner;            /* InnerRecord count                          */
+  uint32_t* inner_restart;     /* [n_inner]                                  */
+  uint32_t* inner_step;        /* [n_inner]                                  */
+  double* inner_monitored;     /* [n_inner] |gamma_{k+1}|                    */
+  double* explicit_residual;   /* [restarts]                                 */
+  double solve_seconds;        /* device time of the solve (CUDA events)     */
+} pgm_report;
+
+typedef struct { /* DeflationRecord, deflation.hpp:24-29 */
+  uint32_t restart;
+  uint32_t r;
+  double mu;
+  double smallest_ritz;
+} pgm_deflation_record;
+
+/* ---- context ----------------------------------------------------------- */
+pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out);
+void pgm_context_destroy(pgm_context* ctx);
+const char* pgm_last_error(const pgm_context* ctx);
+pgm_status pgm_context_partition(const pgm_context* ctx, pgm_partition* out);
+/* partition_rows(mesh, p)[w] without a context (parallel.cpp:50-71). */
+pgm_status pgm_partition_rows(uint32_t n_axis, uint32_t p, uint32_t w, pgm_partition* out);
+/* Device stream the library enqueues on (cudaStream_t), for callers that
+ * time or order work around it. */
+void* pgm_context_stream(pgm_context* ctx);
+
+/* ---- matrix ------------------------------------------------------------ */
+pgm_status pgm_matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags,
+                             pgm_matrix** out);
+pgm_status pgm_matrix_update_values(pgm_matrix* a, const double* values, int32_t flags);
+void pgm_matrix_destroy(pgm_matrix* a);
+pgm_status pgm_matrix_info(const pgm_matrix* a, uint32_t* n, uint64_t* nnz,
+                           uint64_t* stored, uint64_t* device_bytes);
+/* y = A x over the owned rows (halo exchange included when world > 1). */
+pgm_status pgm_spmv(pgm_matrix* a, const double* x, double* y, int32_t flags);
+
+/* ---- deflation preconditioner -------------------------------------------- */
+pgm_status pgm_deflator_create(pgm_context* ctx, const pgm_deflation_config* cfg,
+                               pgm_deflator** out);
+void pgm_deflator_destroy(pgm_deflator* d);
+pgm_status pgm_deflator_reset(pgm_deflator* d);
+pgm_status pgm_deflator_info(pgm_deflator* d, uint32_t* rank, double* mu, uint32_t* skipped,
+                             uint32_t* n_history);
+pgm_status pgm_deflator_history(pgm_deflator* d, pgm_deflation_record* out, uint32_t cap);
+/* U (n_own x rank, column-major) and T (rank x rank, column-major). */
+pgm_status pgm_deflator_basis(pgm_deflator* d, double* U, double* T);
+/* Deflator::push_vector with opA = spmv(a) (deflation.cpp:123-184). */
+pgm_status pgm_deflator_push(pgm_deflator* d, pgm_matrix* a, const double* candidate,
+                             int32_t flags, int32_t* accepted);
+pgm_status pgm_deflator_truncate(pgm_deflator* d);
+pgm_status pgm_deflator_observe_ritz(pgm_deflator* d, double value);
+/* w = v + U(|mu| T^{-1} - I) U^T v (deflation.cpp:104-117). */
+pgm_status pgm_deflator_apply(pgm_deflator* d, const double* v, double* w, int32_t flags);
+
+/* ---- the solve ----------------------------------------------------------- */
+/* deflated_gmres when d != NULL, plain gmres_restarted otherwise.  x holds the
+ * initial guess on entry and the iterate on return; b and x cover the owned
+ * rows.  rep may be NULL. */
+pgm_status pgm_solve(pgm_context* ctx, pgm_matrix* a, pgm_deflator* d, const double* b,
+                     double* x, const pgm_gmres_config* cfg, int32_t flags, pgm_report* rep);
+void pgm_report_free(pgm_report* rep);
+
+/* Kernel launches of the last pgm_solve (evidence for the bench). */
+uint64_t pgm_context_launch_count(const pgm_context* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PGMRES_H_ */

@@ -1,0 +1,15 @@
+"""B200-native deflated PGMRES (arXiv 1906.04051 linear-solve path).
+
+The product is libpgmres.so (hand-written sm_100a CUDA + C ABI, see
+include/pgmres.h); this package is the host-side mirror of the reference's
+solver API over that ABI.
+"""
+from .dgmres import (CsrMatrix, DeflationConfig, DeflationRecord, Deflator, DeviceCsr,
+                     DeviceError, DeviceExecutor, GmresConfig, GmresError, GmresReport,
+                     InnerRecord, deflated_gmres, gmres_restarted)
+
+__all__ = [
+    "CsrMatrix", "DeflationConfig", "DeflationRecord", "Deflator", "DeviceCsr", "DeviceError",
+    "DeviceExecutor", "GmresConfig", "GmresError", "GmresReport", "InnerRecord",
+    "deflated_gmres", "gmres_restarted",
+]

@@ -1,0 +1,155 @@
+// Shared device-side definitions of libpgmres: state structs, launch geometry,
+// deterministic two-level grid reductions.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pgm {
+
+// ---- launch geometry -------------------------------------------------------
+constexpr int TILE = 512;             // rows per SpMV tile (SELL sort window)
+constexpr int SPT = TILE / 32;        // 32-row slices per tile
+constexpr int SPMV_THREADS = 256;
+constexpr int SPMV_UNROLL = 8;
+constexpr int SW_THREADS = 128;       // sweep block: one row per thread
+constexpr int CH = SW_THREADS;        // rows per sweep chunk
+constexpr int GROUP = 16;             // first-level reduction group (blocks)
+constexpr int MAX_M = 112;            // Ritz harvest keeps [H | H^-1] in smem
+constexpr int MAX_R1 = 32;            // r_max + 1 bound of the register fast path
+constexpr int RITZ_THREADS = 256;
+
+// ---- device state ------------------------------------------------------------
+// Per-solve GMRES control word (gmres.cpp:132-218 loop variables + GmresReport
+// scalars).  Lives in device memory; the host reads it once per restart.
+struct GState {
+  int active;       // inner loop of the current cycle still running
+  int done;         // solve finished (converged, max restarts, or error)
+  int error;        // pgm_status code
+  int err_restart, err_step;
+  int restart;      // current 0-based cycle
+  int steps;        // Arnoldi steps completed in the current cycle
+  int lucky;        // cycle ended on h < breakdown_scale * beta
+  int converged, breakdown, restarts, n_inner;
+  unsigned long long total_inner;
+  double beta0, beta, beta_cycle, final_relative;
+  // configuration (GmresConfig)
+  int m, max_restarts, fixed, harvest;
+  double rel_tol, breakdown_scale;
+};
+
+// Deflator state (deflation.hpp:78-88) kept on the device across solves.
+struct DState {
+  int r, skipped, n_hist, hist_cap;
+  double mu;
+  int r_max, drop, inv_maxit, pow_maxit;
+  double accept_tol, inv_tol;
+  // restart-harvest pipeline (update_from_restart / push_vector)
+  int push_ok;      // candidate still alive
+  int rotate;       // truncation produced Q; U, AU need rotating
+  int r0;           // rank before truncation (columns of Q)
+  int trunc_fail;   // eigen decomposition failed (stderr in the reference)
+  double theta, norm_in, pscale;
+};
+
+struct Params {
+  GState* g;
+  DState* d;
+  // GMRES small arrays (m-sized, device)
+  double *s;                      // lazy scale of stored basis column W_l: v_l = s_l W_l
+  double *h_orig, *h_rot;         // (m+1) x m column-major
+  double *gv, *cs, *sn;           // rotated rhs, Givens
+  double *h1, *coefA, *coefB;     // CGS2 pass coefficients
+  double *tU;                     // (m+1) x R1: U^T v_l for every basis vector
+  double *c;                      // deflation coefficients for the next apply
+  double *xc, *cx;                // x update: V y and U c' coefficients
+  double *zl;                     // Ritz lift coefficients (V z)
+  uint32_t *rec_restart, *rec_step;
+  double *rec_mon, *expl;
+  // deflation small arrays (R1-sized)
+  double *T, *Tinv, *Q, *proj, *dwork;
+  int* iwork;
+  uint32_t *hist_restart, *hist_r;
+  double *hist_mu, *hist_theta;
+  // n-sized vectors: each a padded buffer of ld doubles, own rows at +lo
+  double *V, *U, *AU, *x, *b, *u;
+  size_t ld;
+  int n, lo, m, R1;
+  // reduction scratch
+  double *part, *gpart;
+  unsigned* cnt;
+  double* red_out;  // world > 1: block-reduced local sums for the allreduce
+  int world;
+};
+
+// ---- reductions ---------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// acc: [nv][32] per-lane accumulators in smem (each value owned by one warp).
+// Every block writes its block sums; the last block of every GROUP sums its
+// group in block order; the last group-reducer sums the groups in order and
+// returns true with red[0..nv) filled.  The summation order depends only on
+// the grid size, so results are identical run to run.
+__device__ __forceinline__ bool grid_reduce(const double* acc, int nv, const Params& P,
+                                            double* red) {
+  __shared__ int s_flag;
+  const int G = gridDim.x, NG = (G + GROUP - 1) / GROUP;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int v = warp; v < nv; v += nw) {
+    const double s = warp_sum(acc[v * 32 + lane]);
+    if (lane == 0) P.part[(size_t)v * G + blockIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  const int grp = blockIdx.x / GROUP;
+  const int g0 = grp * GROUP;
+  const int gsize = min(GROUP, G - g0);
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(&P.cnt[1 + grp], 1u);
+    s_flag = (t == (unsigned)(gsize - 1));
+  }
+  __syncthreads();
+  if (!s_flag) return false;
+  __threadfence();
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    double s = 0.0;
+    for (int bb = g0; bb < g0 + gsize; ++bb) s += __ldcg(&P.part[(size_t)v * G + bb]);
+    P.gpart[(size_t)v * NG + grp] = s;
+  }
+  if (threadIdx.x == 0) P.cnt[1 + grp] = 0;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(&P.cnt[0], 1u);
+    s_flag = (t == (unsigned)(NG - 1));
+  }
+  __syncthreads();
+  if (!s_flag) return false;
+  __threadfence();
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < NG; ++q) s += __ldcg(&P.gpart[(size_t)v * NG + q]);
+    red[v] = s;
+  }
+  if (threadIdx.x == 0) P.cnt[0] = 0;
+  __syncthreads();
+  return true;
+}
+
+// Block-wide sum (fixed order), result broadcast to every thread.
+__device__ __forceinline__ double block_sum(double v, double* scratch32) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch32[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < nw; ++w) s += scratch32[w];
+  return s;
+}
+
+}  // namespace pgm

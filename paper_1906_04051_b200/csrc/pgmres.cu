@@ -1,0 +1,1179 @@
+// libpgmres: B200-native deflated PGMRES behind the C ABI of include/pgmres.h.
+//
+// Host orchestration only: every vector operation of the hot path runs in the
+// kernels of kernels.cuh; the host enqueues one restart cycle at a time and
+// reads back a small status word once per restart (no per-step round trip).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/pgmres.h"
+#include "kernels.cuh"
+#include "nccl_lite.h"
+
+using namespace pgm;
+
+namespace {
+
+thread_local std::string g_tls_err;
+
+struct Status {  // pgm_status + message
+  pgm_status code = PGM_OK;
+  std::string msg;
+};
+
+#define CU(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      return Status{PGM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};     \
+    }                                                                                   \
+  } while (0)
+
+#define TRY(expr)                 \
+  do {                            \
+    Status s_ = (expr);           \
+    if (s_.code != PGM_OK) return s_; \
+  } while (0)
+
+Status einval(const std::string& m) { return Status{PGM_EINVAL, m}; }
+
+template <class T>
+Status dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return Status{PGM_ENOMEM, std::string("cudaMalloc(") + std::to_string(count * sizeof(T)) +
+                                  " B): " + cudaGetErrorString(e)};
+  }
+  return {};
+}
+template <class T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+size_t round_up(size_t a, size_t b) { return (a + b - 1) / b * b; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct pgm_deflator;
+
+struct pgm_context {
+  int device = 0, rank = 0, world = 1;
+  uint32_t n_axis = 0, n_global = 0;
+  pgm_partition part{};
+  size_t n = 0, lo = 0, hi = 0, ld = 0;
+  cudaStream_t stream = nullptr;
+  int nsm = 148;
+  std::string err;
+  uint64_t launches = 0;
+  // reduction scratch
+  double *part_buf = nullptr, *gpart_buf = nullptr, *red_out = nullptr;
+  unsigned* cnt = nullptr;
+  int gmax = 0, nvmax = 0;
+  // GMRES workspace
+  int ws_m = 0, ws_maxr = 0;
+  double *V = nullptr, *x = nullptr, *b = nullptr, *tmp = nullptr;
+  double *s = nullptr, *h_orig = nullptr, *h_rot = nullptr, *gv = nullptr, *cs = nullptr,
+         *sn = nullptr, *h1 = nullptr, *coefA = nullptr, *coefB = nullptr, *tU = nullptr,
+         *c = nullptr, *xc = nullptr, *cx = nullptr, *zl = nullptr;
+  uint32_t *rec_restart = nullptr, *rec_step = nullptr;
+  double *rec_mon = nullptr, *expl = nullptr;
+  int ws_R1 = 0;
+  GState* g = nullptr;
+  GState* h_status = nullptr;  // pinned
+  pgm_deflator* dummy = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // multi-GPU
+  void* nccl = nullptr;
+};
+
+struct pgm_matrix {
+  pgm_context* ctx = nullptr;
+  uint32_t n = 0;
+  uint64_t nnz = 0, stored = 0;
+  int nslices = 0, ntiles = 0;
+  unsigned long long* sptr = nullptr;
+  unsigned* lane_len = nullptr;
+  unsigned short* lane_row = nullptr;
+  double* val = nullptr;
+  unsigned* col = nullptr;
+  unsigned* rp = nullptr;      // device CSR row_ptr (kept for value updates)
+  double* vstage = nullptr;    // device CSR values staging
+  unsigned col_shift = 0;
+  Sell view() const {
+    Sell S;
+    S.sptr = sptr;
+    S.lane_len = lane_len;
+    S.lane_row = lane_row;
+    S.val = val;
+    S.col = col;
+    S.ntiles = ntiles;
+    S.n = (int)n;
+    return S;
+  }
+};
+
+struct pgm_deflator {
+  pgm_context* ctx = nullptr;
+  pgm_deflation_config cfg{};
+  int R1 = 0;
+  DState* d = nullptr;
+  double *U = nullptr, *AU = nullptr, *u = nullptr;
+  double *T = nullptr, *Tinv = nullptr, *Q = nullptr, *proj = nullptr, *dwork = nullptr;
+  int* iwork = nullptr;
+  uint32_t *hist_restart = nullptr, *hist_r = nullptr;
+  double *hist_mu = nullptr, *hist_theta = nullptr;
+  int hist_cap = 0;
+  bool dummy = false;
+};
+
+namespace {
+
+pgm_status fail(pgm_context* ctx, const Status& s) {
+  if (ctx) ctx->err = s.msg;
+  g_tls_err = s.msg;
+  return s.code;
+}
+
+// ---------------------------------------------------------------------------
+// Launch geometry
+template <class K>
+int occupancy(K kernel, int threads, size_t smem) {
+  int nb = 0;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem);
+  return std::max(1, nb);
+}
+
+constexpr int MAX_BLOCKS_PER_SM = 4;  // bounds the grid-reduction tail
+
+size_t spmv_smem(int nv) { return sizeof(double) * (EPI_SMALL + 2 * TILE + 33 * (size_t)nv); }
+size_t sweep_smem(int np, int np2, int nv, bool staged) {
+  return sizeof(double) *
+         ((size_t)np + np2 + CH + 33 * (size_t)nv + (staged ? (size_t)np * CH : 0));
+}
+
+template <class Epi>
+Status launch_spmv(pgm_context* ctx, const pgm_matrix* A, const Params& P, const Epi& E,
+                   int nvmax) {
+  const size_t smem = spmv_smem(nvmax);
+  const int occ = std::min(MAX_BLOCKS_PER_SM, occupancy(k_spmv<Epi>, SPMV_THREADS, smem));
+  const int G = std::max(1, std::min(A->ntiles, occ * ctx->nsm));
+  k_spmv<Epi><<<G, SPMV_THREADS, smem, ctx->stream>>>(A->view(), P, E);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return {};
+}
+
+template <int MODE>
+Status launch_sweep(pgm_context* ctx, const Params& P, int k, int np, int np2, int nv,
+                    bool staged) {
+  const size_t smem = sweep_smem(np, np2, nv, staged);
+  const int occ = std::min(MAX_BLOCKS_PER_SM, occupancy(k_sweep<MODE>, SW_THREADS, smem));
+  const int nchunks = (int)((ctx->n + CH - 1) / CH);
+  const int G = std::max(1, std::min(nchunks, occ * ctx->nsm));
+  k_sweep<MODE><<<G, SW_THREADS, smem, ctx->stream>>>(P, k);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return {};
+}
+
+// ---------------------------------------------------------------------------
+// Context-owned buffers
+
+Status ensure_reduction(pgm_context* ctx, int nv) {
+  const int gmax = ctx->nsm * 8;
+  if (ctx->part_buf && ctx->nvmax >= nv && ctx->gmax >= gmax) return {};
+  dfree(ctx->part_buf);
+  dfree(ctx->gpart_buf);
+  dfree(ctx->cnt);
+  dfree(ctx->red_out);
+  ctx->nvmax = std::max(nv, 2 * MAX_R1 + MAX_M + 8);
+  ctx->gmax = gmax;
+  const int ng = (gmax + GROUP - 1) / GROUP;
+  TRY(dalloc(&ctx->part_buf, (size_t)ctx->nvmax * gmax));
+  TRY(dalloc(&ctx->gpart_buf, (size_t)ctx->nvmax * ng));
+  TRY(dalloc(&ctx->cnt, (size_t)ng + 1));
+  TRY(dalloc(&ctx->red_out, (size_t)ctx->nvmax));
+  CU(cudaMemset(ctx->cnt, 0, sizeof(unsigned) * (ng + 1)));
+  return {};
+}
+
+void free_workspace(pgm_context* ctx) {
+  dfree(ctx->V);
+  dfree(ctx->s);
+  dfree(ctx->h_orig);
+  dfree(ctx->h_rot);
+  dfree(ctx->gv);
+  dfree(ctx->cs);
+  dfree(ctx->sn);
+  dfree(ctx->h1);
+  dfree(ctx->coefA);
+  dfree(ctx->coefB);
+  dfree(ctx->tU);
+  dfree(ctx->c);
+  dfree(ctx->xc);
+  dfree(ctx->cx);
+  dfree(ctx->zl);
+  dfree(ctx->rec_restart);
+  dfree(ctx->rec_step);
+  dfree(ctx->rec_mon);
+  dfree(ctx->expl);
+  ctx->ws_m = ctx->ws_maxr = ctx->ws_R1 = 0;
+}
+
+Status ensure_workspace(pgm_context* ctx, int m, int max_restarts, int R1) {
+  if (ctx->V && ctx->ws_m == m && ctx->ws_maxr >= max_restarts && ctx->ws_R1 >= R1) return {};
+  free_workspace(ctx);
+  const size_t ld = ctx->ld;
+  TRY(dalloc(&ctx->V, (size_t)(m + 1) * ld));
+  CU(cudaMemset(ctx->V, 0, sizeof(double) * (m + 1) * ld));
+  const size_t hm = (size_t)(m + 1) * m;
+  TRY(dalloc(&ctx->s, m + 2));
+  TRY(dalloc(&ctx->h_orig, hm));
+  TRY(dalloc(&ctx->h_rot, hm));
+  CU(cudaMemset(ctx->h_orig, 0, sizeof(double) * hm));
+  CU(cudaMemset(ctx->h_rot, 0, sizeof(double) * hm));
+  TRY(dalloc(&ctx->gv, m + 2));
+  TRY(dalloc(&ctx->cs, m + 1));
+  TRY(dalloc(&ctx->sn, m + 1));
+  TRY(dalloc(&ctx->h1, m + 2));
+  TRY(dalloc(&ctx->coefA, m + 2));
+  TRY(dalloc(&ctx->coefB, m + 2));
+  TRY(dalloc(&ctx->tU, (size_t)(m + 2) * R1));
+  TRY(dalloc(&ctx->c, R1 + 1));
+  TRY(dalloc(&ctx->xc, m + 2));
+  TRY(dalloc(&ctx->cx, R1 + 1));
+  TRY(dalloc(&ctx->zl, m + 2));
+  const size_t cap = (size_t)std::max(1, max_restarts) * m;
+  TRY(dalloc(&ctx->rec_restart, cap));
+  TRY(dalloc(&ctx->rec_step, cap));
+  TRY(dalloc(&ctx->rec_mon, cap));
+  TRY(dalloc(&ctx->expl, std::max(1, max_restarts)));
+  ctx->ws_m = m;
+  ctx->ws_maxr = max_restarts;
+  ctx->ws_R1 = R1;
+  return {};
+}
+
+Status defl_alloc_vectors(pgm_deflator* d) {
+  if (d->U) return {};
+  pgm_context* ctx = d->ctx;
+  const size_t ld = ctx->ld;
+  const int R1 = d->dummy ? 1 : d->R1;
+  TRY(dalloc(&d->U, (size_t)R1 * ld));
+  TRY(dalloc(&d->AU, (size_t)R1 * ld));
+  TRY(dalloc(&d->u, ld));
+  CU(cudaMemset(d->U, 0, sizeof(double) * R1 * ld));
+  CU(cudaMemset(d->AU, 0, sizeof(double) * R1 * ld));
+  CU(cudaMemset(d->u, 0, sizeof(double) * ld));
+  return {};
+}
+
+Status defl_ensure_hist(pgm_deflator* d, int need) {
+  if (need <= d->hist_cap) return {};
+  int cap = std::max(need, 2 * d->hist_cap + 64);
+  uint32_t *hr = nullptr, *hrr = nullptr;
+  double *hm = nullptr, *ht = nullptr;
+  TRY(dalloc(&hr, cap));
+  TRY(dalloc(&hrr, cap));
+  TRY(dalloc(&hm, cap));
+  TRY(dalloc(&ht, cap));
+  DState hs;
+  CU(cudaMemcpy(&hs, d->d, sizeof(DState), cudaMemcpyDeviceToHost));
+  const int keep = std::min(hs.n_hist, d->hist_cap);
+  if (keep > 0) {
+    CU(cudaMemcpy(hr, d->hist_restart, 4 * keep, cudaMemcpyDeviceToDevice));
+    CU(cudaMemcpy(hrr, d->hist_r, 4 * keep, cudaMemcpyDeviceToDevice));
+    CU(cudaMemcpy(hm, d->hist_mu, 8 * keep, cudaMemcpyDeviceToDevice));
+    CU(cudaMemcpy(ht, d->hist_theta, 8 * keep, cudaMemcpyDeviceToDevice));
+  }
+  dfree(d->hist_restart);
+  dfree(d->hist_r);
+  dfree(d->hist_mu);
+  dfree(d->hist_theta);
+  d->hist_restart = hr;
+  d->hist_r = hrr;
+  d->hist_mu = hm;
+  d->hist_theta = ht;
+  d->hist_cap = cap;
+  hs.hist_cap = cap;
+  CU(cudaMemcpy(&d->d->hist_cap, &cap, sizeof(int), cudaMemcpyHostToDevice));
+  return {};
+}
+
+Params make_params(pgm_context* ctx, pgm_deflator* d) {
+  Params P{};
+  P.g = ctx->g;
+  P.d = d->d;
+  P.s = ctx->s;
+  P.h_orig = ctx->h_orig;
+  P.h_rot = ctx->h_rot;
+  P.gv = ctx->gv;
+  P.cs = ctx->cs;
+  P.sn = ctx->sn;
+  P.h1 = ctx->h1;
+  P.coefA = ctx->coefA;
+  P.coefB = ctx->coefB;
+  P.tU = ctx->tU;
+  P.c = ctx->c;
+  P.xc = ctx->xc;
+  P.cx = ctx->cx;
+  P.zl = ctx->zl;
+  P.rec_restart = ctx->rec_restart;
+  P.rec_step = ctx->rec_step;
+  P.rec_mon = ctx->rec_mon;
+  P.expl = ctx->expl;
+  P.T = d->T;
+  P.Tinv = d->Tinv;
+  P.Q = d->Q;
+  P.proj = d->proj;
+  P.dwork = d->dwork;
+  P.iwork = d->iwork;
+  P.hist_restart = d->hist_restart;
+  P.hist_r = d->hist_r;
+  P.hist_mu = d->hist_mu;
+  P.hist_theta = d->hist_theta;
+  P.V = ctx->V;
+  P.U = d->U;
+  P.AU = d->AU;
+  P.x = ctx->x;
+  P.b = ctx->b;
+  P.u = d->u;
+  P.ld = ctx->ld;
+  P.n = (int)ctx->n;
+  P.lo = (int)ctx->lo;
+  P.m = ctx->ws_m;
+  P.R1 = d->R1;
+  P.part = ctx->part_buf;
+  P.gpart = ctx->gpart_buf;
+  P.cnt = ctx->cnt;
+  P.red_out = ctx->red_out;
+  P.world = ctx->world;
+  return P;
+}
+
+// Small-state workspace for the standalone deflator entry points.
+Status ensure_min_workspace(pgm_context* ctx, int R1) {
+  if (ctx->V && ctx->ws_R1 >= R1) return {};
+  return ensure_workspace(ctx, std::max(1, ctx->ws_m), std::max(1, ctx->ws_maxr),
+                          std::max(R1, ctx->ws_R1));
+}
+
+Status set_gstate_idle(pgm_context* ctx) {
+  GState gs{};
+  gs.harvest = 0;
+  CU(cudaMemcpyAsync(ctx->g, &gs, sizeof(GState), cudaMemcpyHostToDevice, ctx->stream));
+  return {};
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU collectives (world > 1): allreduce of the block-reduced sums,
+// then the scalar finisher on every rank.
+Status allreduce_red(pgm_context* ctx, int nv);
+Status halo_exchange(pgm_context* ctx, double* vec);
+
+template <int KIND>
+Status finish_global(pgm_context* ctx, const Params& P, int k, int nv) {
+  if (ctx->world == 1) return {};
+  TRY(allreduce_red(ctx, nv));
+  k_finish<KIND><<<1, 32, 0, ctx->stream>>>(P, k);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return {};
+}
+
+// One restart cycle of the solve: m Arnoldi steps (3 fused kernels each), the
+// x update, the deflation harvest and the explicit residual.
+Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Params& P,
+                     bool harvest) {
+  const int m = ctx->ws_m;
+  const int R1 = d->R1;
+  for (int k = 0; k < m; ++k) {
+    if (ctx->world > 1) TRY(halo_exchange(ctx, ctx->V + (size_t)k * ctx->ld));
+    StepEpi se{k};
+    TRY(launch_spmv(ctx, A, P, se, m + 1));
+    TRY(finish_global<100>(ctx, P, k, k + 1));
+    TRY(launch_sweep<SW_CGS2_B>(ctx, P, k, m + 1, 0, m + 1, true));
+    TRY(finish_global<SW_CGS2_B>(ctx, P, k, k + 1));
+    TRY(launch_sweep<SW_CGS2_C>(ctx, P, k, m + 1, 0, R1 + 1, false));
+    TRY(finish_global<SW_CGS2_C>(ctx, P, k, -1));
+  }
+  TRY(launch_sweep<SW_XUPDATE>(ctx, P, 0, m, R1, 0, false));
+  if (harvest) {
+    const size_t rsmem = sizeof(double) * (2 * (size_t)m * m + 4 * m);
+    if (rsmem > 48 * 1024)
+      CU(cudaFuncSetAttribute(k_ritz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
+    k_ritz<<<1, RITZ_THREADS, rsmem, ctx->stream>>>(P);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    TRY(launch_sweep<SW_PUSH1>(ctx, P, 1, m, 0, R1 + 1, false));
+    TRY(finish_global<SW_PUSH1>(ctx, P, 1, -1));
+    TRY(launch_sweep<SW_PUSH2>(ctx, P, 0, R1, 0, R1, true));
+    TRY(finish_global<SW_PUSH2>(ctx, P, 0, -1));
+    TRY(launch_sweep<SW_PUSH3>(ctx, P, 0, R1, 0, 1, false));
+    TRY(finish_global<SW_PUSH3>(ctx, P, 0, -1));
+    if (ctx->world > 1) TRY(halo_exchange(ctx, d->u));
+    TRY(launch_spmv(ctx, A, P, PushEpi{}, 2 * R1 + 1));
+    TRY(finish_global<102>(ctx, P, 0, -1));
+    k_rotate<true><<<ctx->nsm * 4, 256, 0, ctx->stream>>>(P);
+    ctx->launches++;
+    CU(cudaGetLastError());
+  }
+  if (ctx->world > 1) TRY(halo_exchange(ctx, ctx->x));
+  TRY(launch_spmv(ctx, A, P, ResidualEpi{0}, R1 + 1));
+  TRY(finish_global<101>(ctx, P, 0, -1));
+  return {};
+}
+
+Status read_status(pgm_context* ctx) {
+  CU(cudaMemcpyAsync(ctx->h_status, ctx->g, sizeof(GState), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return {};
+}
+
+Status error_of(const GState& gs) {
+  switch (gs.error) {
+    case 0:
+      return {};
+    case 2:
+      if (gs.err_restart < 0) return Status{PGM_ENONFINITE, "gmres: initial residual is not finite"};
+      if (gs.err_step < 0)
+        return Status{PGM_ENONFINITE, "gmres: non-finite residual after restart " +
+                                          std::to_string(gs.err_restart)};
+      return Status{PGM_ENONFINITE, "gmres: non-finite Arnoldi coefficient at restart " +
+                                        std::to_string(gs.err_restart) + ", step " +
+                                        std::to_string(gs.err_step)};
+    case 3:
+      return Status{PGM_ESINGULAR, "gmres: singular projection in least squares"};
+    default:
+      return Status{(pgm_status)gs.error, "device error"};
+  }
+}
+
+Status copy_in(pgm_context* ctx, double* dst_own, const double* src, size_t n, int32_t flags) {
+  CU(cudaMemcpyAsync(dst_own, src, n * sizeof(double),
+                     (flags & PGM_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     ctx->stream));
+  return {};
+}
+Status copy_out(pgm_context* ctx, double* dst, const double* src_own, size_t n, int32_t flags) {
+  CU(cudaMemcpyAsync(dst, src_own, n * sizeof(double),
+                     (flags & PGM_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  return {};
+}
+
+Status solve_impl(pgm_context* ctx, pgm_matrix* A, pgm_deflator* dflt, const double* b, double* x,
+                  const pgm_gmres_config* cfg, int32_t flags, pgm_report* rep) {
+  if (!cfg) return einval("pgm_solve: null config");
+  if (cfg->m == 0) return einval("GmresWorkspace: m must be positive");
+  if (!A || A->ctx != ctx) return einval("pgm_solve: matrix belongs to another context");
+  if (A->n != ctx->n) return einval("pgm_solve: matrix rows do not match the partition");
+  const bool harvest = dflt != nullptr;
+  if (harvest && cfg->m > (uint32_t)MAX_M)
+    return einval("pgm_solve: deflated restart length m > " + std::to_string(MAX_M) +
+                  " is not supported on the device harvest path");
+  if (!harvest && cfg->m > 4096) return einval("pgm_solve: m too large");
+  pgm_deflator* d = harvest ? dflt : ctx->dummy;
+  if (d->ctx != ctx) return einval("pgm_solve: deflator belongs to another context");
+  const int m = (int)cfg->m;
+  const int maxr = (int)cfg->max_restarts;
+  TRY(ensure_reduction(ctx, std::max(m + 1, 2 * d->R1 + 1)));
+  TRY(ensure_workspace(ctx, m, maxr, std::max(d->R1, 1)));
+  TRY(defl_alloc_vectors(d));
+  if (harvest) {
+    DState hs;
+    CU(cudaMemcpy(&hs, d->d, sizeof(DState), cudaMemcpyDeviceToHost));
+    TRY(defl_ensure_hist(d, hs.n_hist + maxr + 1));
+  }
+  const size_t n = ctx->n;
+  TRY(copy_in(ctx, ctx->b + ctx->lo, b, n, flags));
+  TRY(copy_in(ctx, ctx->x + ctx->lo, x, n, flags));
+  GState gs{};
+  gs.m = m;
+  gs.max_restarts = maxr;
+  gs.fixed = cfg->fixed_iterations != 0;
+  gs.harvest = harvest ? 1 : 0;
+  gs.rel_tol = cfg->rel_tol;
+  gs.breakdown_scale = cfg->breakdown_scale;
+  CU(cudaMemcpyAsync(ctx->g, &gs, sizeof(GState), cudaMemcpyHostToDevice, ctx->stream));
+  const Params P = make_params(ctx, d);
+  ctx->launches = 0;
+  CU(cudaEventRecord(ctx->ev0, ctx->stream));
+  if (ctx->world > 1) TRY(halo_exchange(ctx, ctx->x));
+  TRY(launch_spmv(ctx, A, P, ResidualEpi{1}, d->R1 + 1));
+  TRY(finish_global<101>(ctx, P, 1, -1));
+  TRY(read_status(ctx));
+  while (!ctx->h_status->done) {
+    TRY(enqueue_cycle(ctx, A, d, P, harvest));
+    TRY(read_status(ctx));
+  }
+  CU(cudaEventRecord(ctx->ev1, ctx->stream));
+  const GState hs = *ctx->h_status;
+  TRY(copy_out(ctx, x, ctx->x + ctx->lo, n, flags));
+  CU(cudaStreamSynchronize(ctx->stream));
+  TRY(error_of(hs));
+  if (rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->beta0 = hs.beta0;
+    rep->restarts = (uint32_t)hs.restarts;
+    rep->total_inner = hs.total_inner;
+    rep->converged = hs.converged;
+    rep->breakdown = hs.breakdown;
+    rep->final_relative = hs.final_relative;
+    rep->n_inner = (uint32_t)hs.n_inner;
+    const size_t ni = std::max<size_t>(1, hs.n_inner), nr = std::max<size_t>(1, hs.restarts);
+    rep->inner_restart = (uint32_t*)std::malloc(4 * ni);
+    rep->inner_step = (uint32_t*)std::malloc(4 * ni);
+    rep->inner_monitored = (double*)std::malloc(8 * ni);
+    rep->explicit_residual = (double*)std::malloc(8 * nr);
+    if (hs.n_inner > 0) {
+      CU(cudaMemcpy(rep->inner_restart, ctx->rec_restart, 4 * hs.n_inner, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(rep->inner_step, ctx->rec_step, 4 * hs.n_inner, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(rep->inner_monitored, ctx->rec_mon, 8 * hs.n_inner, cudaMemcpyDeviceToHost));
+    }
+    if (hs.restarts > 0)
+      CU(cudaMemcpy(rep->explicit_residual, ctx->expl, 8 * hs.restarts, cudaMemcpyDeviceToHost));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    rep->solve_seconds = 1e-3 * ms;
+  }
+  return {};
+}
+
+// ---------------------------------------------------------------------------
+// Matrix upload: CSR (owned rows, global columns) -> SELL-32 tiles.
+struct SliceLayout {
+  std::vector<unsigned long long> sptr;
+  std::vector<unsigned> lane_len;
+  std::vector<unsigned short> lane_row;
+};
+
+SliceLayout build_layout(const uint32_t* rp, uint32_t n) {
+  SliceLayout L;
+  const int ntiles = (int)((n + TILE - 1) / TILE);
+  const size_t nslices = (size_t)ntiles * SPT;
+  L.sptr.assign(nslices + 1, 0);
+  L.lane_len.assign(nslices * 32, 0);
+  L.lane_row.assign(nslices * 32, 0xFFFF);
+  std::vector<int> order(TILE);
+  unsigned long long off = 0;
+  for (int t = 0; t < ntiles; ++t) {
+    const uint32_t r0 = (uint32_t)t * TILE;
+    const int rows = (int)std::min<uint32_t>(TILE, n - r0);
+    for (int i = 0; i < rows; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.begin() + rows, [&](int a, int b) {
+      return (rp[r0 + a + 1] - rp[r0 + a]) > (rp[r0 + b + 1] - rp[r0 + b]);
+    });
+    for (int sl = 0; sl < SPT; ++sl) {
+      const size_t s = (size_t)t * SPT + sl;
+      unsigned Lmax = 0;
+      for (int lane = 0; lane < 32; ++lane) {
+        const int idx = sl * 32 + lane;
+        if (idx < rows) {
+          const int row = order[idx];
+          const unsigned len = rp[r0 + row + 1] - rp[r0 + row];
+          L.lane_len[s * 32 + lane] = len;
+          L.lane_row[s * 32 + lane] = (unsigned short)row;
+          Lmax = std::max(Lmax, len);
+        }
+      }
+      L.sptr[s] = off;
+      off += 32ull * Lmax;
+    }
+  }
+  L.sptr[nslices] = off;
+  return L;
+}
+
+Status matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags, pgm_matrix** out) {
+  if (!a || !out) return einval("pgm_matrix_upload: null argument");
+  if (a->n != ctx->n)
+    return einval("pgm_matrix_upload: view has " + std::to_string(a->n) + " rows, partition owns " +
+                  std::to_string(ctx->n));
+  const bool dev = (flags & PGM_DEVICE_PTRS) != 0;
+  std::vector<uint32_t> rp_h(a->n + 1);
+  if (dev) {
+    CU(cudaMemcpy(rp_h.data(), a->row_ptr, 4 * (a->n + 1), cudaMemcpyDeviceToHost));
+  } else {
+    std::memcpy(rp_h.data(), a->row_ptr, 4 * (a->n + 1));
+  }
+  if (rp_h[0] != 0 || rp_h[a->n] != a->nnz)
+    return einval("pgm_matrix_upload: row_ptr must start at 0 and end at nnz");
+  for (uint32_t i = 0; i < a->n; ++i)
+    if (rp_h[i + 1] < rp_h[i]) return einval("pgm_matrix_upload: row_ptr not monotone");
+  SliceLayout L = build_layout(rp_h.data(), a->n);
+  auto* M = new pgm_matrix();
+  M->ctx = ctx;
+  M->n = a->n;
+  M->nnz = a->nnz;
+  M->ntiles = (int)((a->n + TILE - 1) / TILE);
+  M->nslices = M->ntiles * SPT;
+  M->stored = L.sptr.back();
+  M->col_shift = ctx->part.row_begin - ctx->part.halo_lo;
+  auto cleanup = [&](Status s) {
+    pgm_matrix_destroy(M);
+    return s;
+  };
+  Status s;
+  if ((s = dalloc(&M->sptr, L.sptr.size())).code) return cleanup(s);
+  if ((s = dalloc(&M->lane_len, L.lane_len.size())).code) return cleanup(s);
+  if ((s = dalloc(&M->lane_row, L.lane_row.size())).code) return cleanup(s);
+  if ((s = dalloc(&M->val, M->stored)).code) return cleanup(s);
+  if ((s = dalloc(&M->col, M->stored)).code) return cleanup(s);
+  if ((s = dalloc(&M->rp, (size_t)a->n + 1)).code) return cleanup(s);
+  if ((s = dalloc(&M->vstage, a->nnz)).code) return cleanup(s);
+  unsigned* cstage = nullptr;
+  if ((s = dalloc(&cstage, a->nnz)).code) return cleanup(s);
+  const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  cudaStream_t st = ctx->stream;
+  cudaError_t e = cudaSuccess;
+  e = e ? e : cudaMemcpyAsync(M->sptr, L.sptr.data(), 8 * L.sptr.size(), cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(M->lane_len, L.lane_len.data(), 4 * L.lane_len.size(), cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(M->lane_row, L.lane_row.data(), 2 * L.lane_row.size(), cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(M->rp, rp_h.data(), 4 * ((size_t)a->n + 1), cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(M->vstage, a->values, 8 * a->nnz, kind, st);
+  e = e ? e : cudaMemcpyAsync(cstage, a->col_idx, 4 * a->nnz, kind, st);
+  if (e != cudaSuccess) {
+    cudaFree(cstage);
+    return cleanup(Status{PGM_ECUDA, std::string("upload: ") + cudaGetErrorString(e)});
+  }
+  const int threads = 256;
+  const size_t blocks = ((size_t)M->nslices * 32 + threads - 1) / threads;
+  if (M->nslices > 0)
+    k_csr_to_sell<<<(unsigned)blocks, threads, 0, st>>>(M->view(), M->val, M->col, M->rp, cstage,
+                                                        M->vstage, M->col_shift, M->nslices, 1);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(cstage);
+  if (e != cudaSuccess)
+    return cleanup(Status{PGM_ECUDA, std::string("csr->sell: ") + cudaGetErrorString(e)});
+  *out = M;
+  return {};
+}
+
+}  // namespace
+
+// ===========================================================================
+// Multi-GPU plumbing (NCCL through a dlopen'ed libnccl: the library carries no
+// link-time dependency, single-GPU use never loads it).
+namespace {
+
+Status allreduce_red(pgm_context* ctx, int nv) {
+  if (!nccl_lite::available() || !ctx->nccl) return Status{PGM_ENCCL, "NCCL not initialised"};
+  if (nccl_lite::allreduce_sum_f64(ctx->red_out, ctx->red_out, (size_t)nv, ctx->nccl, ctx->stream) != 0)
+    return Status{PGM_ENCCL, "ncclAllReduce failed"};
+  return {};
+}
+
+// Exchange the two boundary planes of `vec` with the z-neighbours: own rows
+// [0, halo) go down into the lower neighbour's halo_hi region and own rows
+// [n - halo, n) go up into the upper neighbour's halo_lo region.
+Status halo_exchange(pgm_context* ctx, double* vec) {
+  if (ctx->world == 1) return {};
+  if (!ctx->nccl) return Status{PGM_ENCCL, "NCCL not initialised"};
+  const size_t lo = ctx->lo, hi = ctx->hi, n = ctx->n;
+  const int below = ctx->rank - 1, above = ctx->rank + 1;
+  if (nccl_lite::group_start() != 0) return Status{PGM_ENCCL, "ncclGroupStart failed"};
+  int rc = 0;
+  if (below >= 0 && lo > 0) {
+    rc |= nccl_lite::send_f64(vec + lo, lo, below, ctx->nccl, ctx->stream);
+    rc |= nccl_lite::recv_f64(vec, lo, below, ctx->nccl, ctx->stream);
+  }
+  if (above < ctx->world && hi > 0) {
+    rc |= nccl_lite::send_f64(vec + lo + n - hi, hi, above, ctx->nccl, ctx->stream);
+    rc |= nccl_lite::recv_f64(vec + lo + n, hi, above, ctx->nccl, ctx->stream);
+  }
+  rc |= nccl_lite::group_end();
+  if (rc) return Status{PGM_ENCCL, "halo exchange failed"};
+  return {};
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+extern "C" {
+
+const char* pgm_last_error(const pgm_context* ctx) {
+  return ctx ? ctx->err.c_str() : g_tls_err.c_str();
+}
+
+pgm_status pgm_partition_rows(uint32_t n_axis, uint32_t p, uint32_t w, pgm_partition* out) {
+  if (!out || p == 0 || p > n_axis || w >= p) {
+    g_tls_err = "partition_rows: need 1 <= p <= n_axis";
+    return PGM_EINVAL;
+  }
+  const uint64_t plane = (uint64_t)n_axis * n_axis;
+  const uint32_t q = n_axis / p, rem = n_axis % p;
+  uint32_t zb = 0;
+  for (uint32_t i = 0; i < w; ++i) zb += q + (i < rem ? 1 : 0);
+  const uint32_t ze = zb + q + (w < rem ? 1 : 0);
+  const uint32_t lo = zb >= 2 ? zb - 2 : 0;
+  const uint32_t hi = std::min(n_axis, ze + 2);
+  out->row_begin = (uint32_t)(zb * plane);
+  out->row_end = (uint32_t)(ze * plane);
+  out->halo_lo = (uint32_t)((zb - lo) * plane);
+  out->halo_hi = (uint32_t)((hi - ze) * plane);
+  return PGM_OK;
+}
+
+pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) {
+  if (!cfg || !out) {
+    g_tls_err = "pgm_context_create: null argument";
+    return PGM_EINVAL;
+  }
+  *out = nullptr;
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world || cfg->n_global == 0) {
+    g_tls_err = "pgm_context_create: bad rank/world/n_global";
+    return PGM_EINVAL;
+  }
+  auto* ctx = new pgm_context();
+  ctx->device = cfg->device;
+  ctx->rank = cfg->rank;
+  ctx->world = cfg->world;
+  ctx->n_axis = cfg->n_axis;
+  ctx->n_global = cfg->n_global;
+  if (cfg->world == 1) {
+    ctx->part = pgm_partition{0, cfg->n_global, 0, 0};
+  } else if (cfg->n_axis > 0) {
+    if ((uint64_t)cfg->n_axis * cfg->n_axis * cfg->n_axis != cfg->n_global) {
+      delete ctx;
+      g_tls_err = "pgm_context_create: n_global != n_axis^3";
+      return PGM_EINVAL;
+    }
+    if (pgm_partition_rows(cfg->n_axis, cfg->world, cfg->rank, &ctx->part) != PGM_OK) {
+      delete ctx;
+      return PGM_EINVAL;
+    }
+  } else {
+    delete ctx;
+    g_tls_err = "pgm_context_create: world > 1 needs the mesh n_axis (z-slab partition)";
+    return PGM_EINVAL;
+  }
+  ctx->n = ctx->part.row_end - ctx->part.row_begin;
+  ctx->lo = ctx->part.halo_lo;
+  ctx->hi = ctx->part.halo_hi;
+  ctx->ld = round_up(ctx->lo + ctx->n + ctx->hi, 32);
+  auto bail = [&](const Status& s) {
+    pgm_status c = fail(nullptr, s);
+    pgm_context_destroy(ctx);
+    return c;
+  };
+  cudaError_t e = cudaSetDevice(cfg->device);
+  if (e != cudaSuccess) return bail(Status{PGM_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)});
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device);
+  ctx->nsm = nsm > 0 ? nsm : 148;
+  e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return bail(Status{PGM_ECUDA, std::string("stream: ") + cudaGetErrorString(e)});
+  cudaEventCreate(&ctx->ev0);
+  cudaEventCreate(&ctx->ev1);
+  Status s;
+  if ((s = dalloc(&ctx->g, 1)).code) return bail(s);
+  if ((e = cudaMallocHost(&ctx->h_status, sizeof(GState))) != cudaSuccess)
+    return bail(Status{PGM_ENOMEM, "pinned status"});
+  std::memset(ctx->h_status, 0, sizeof(GState));
+  if ((s = dalloc(&ctx->x, ctx->ld)).code) return bail(s);
+  if ((s = dalloc(&ctx->b, ctx->ld)).code) return bail(s);
+  if ((s = dalloc(&ctx->tmp, ctx->ld)).code) return bail(s);
+  cudaMemset(ctx->x, 0, 8 * ctx->ld);
+  cudaMemset(ctx->b, 0, 8 * ctx->ld);
+  cudaMemset(ctx->tmp, 0, 8 * ctx->ld);
+  if ((s = ensure_reduction(ctx, 2 * MAX_R1 + MAX_M + 8)).code) return bail(s);
+  if ((s = set_gstate_idle(ctx)).code) return bail(s);
+  if (cfg->world > 1) {
+    if (!nccl_lite::available()) return bail(Status{PGM_ENCCL, "libnccl.so.2 not loadable"});
+    if (!cfg->nccl_id) return bail(Status{PGM_EINVAL, "world > 1 needs an ncclUniqueId"});
+    if (nccl_lite::comm_init_rank(&ctx->nccl, cfg->world, cfg->nccl_id, cfg->rank) != 0)
+      return bail(Status{PGM_ENCCL, "ncclCommInitRank failed"});
+  }
+  // dummy deflator (r = 0 forever) for plain gmres_restarted solves
+  pgm_deflation_config dc{1, 1, 1e-8, 1, 1e-10, 1};
+  pgm_deflator* dd = nullptr;
+  if (pgm_deflator_create(ctx, &dc, &dd) != PGM_OK) {
+    pgm_status c = PGM_ENOMEM;
+    pgm_context_destroy(ctx);
+    return c;
+  }
+  dd->dummy = true;
+  ctx->dummy = dd;
+  cudaDeviceSynchronize();
+  *out = ctx;
+  return PGM_OK;
+}
+
+void pgm_context_destroy(pgm_context* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->dummy) pgm_deflator_destroy(ctx->dummy);
+  free_workspace(ctx);
+  dfree(ctx->x);
+  dfree(ctx->b);
+  dfree(ctx->tmp);
+  dfree(ctx->g);
+  dfree(ctx->part_buf);
+  dfree(ctx->gpart_buf);
+  dfree(ctx->cnt);
+  dfree(ctx->red_out);
+  if (ctx->h_status) cudaFreeHost(ctx->h_status);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->nccl) nccl_lite::comm_destroy(ctx->nccl);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+pgm_status pgm_context_partition(const pgm_context* ctx, pgm_partition* out) {
+  if (!ctx || !out) return PGM_EINVAL;
+  *out = ctx->part;
+  return PGM_OK;
+}
+
+void* pgm_context_stream(pgm_context* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+uint64_t pgm_context_launch_count(const pgm_context* ctx) { return ctx ? ctx->launches : 0; }
+
+pgm_status pgm_matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags,
+                             pgm_matrix** out) {
+  if (!ctx) return PGM_EINVAL;
+  cudaSetDevice(ctx->device);
+  Status s = matrix_upload(ctx, a, flags, out);
+  return s.code ? fail(ctx, s) : PGM_OK;
+}
+
+pgm_status pgm_matrix_update_values(pgm_matrix* a, const double* values, int32_t flags) {
+  if (!a) return PGM_EINVAL;
+  pgm_context* ctx = a->ctx;
+  cudaStream_t st = ctx->stream;
+  cudaError_t e = cudaMemcpyAsync(a->vstage, values, 8 * a->nnz,
+                                  (flags & PGM_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice
+                                                            : cudaMemcpyHostToDevice,
+                                  st);
+  if (e == cudaSuccess && a->nslices > 0) {
+    const size_t blocks = ((size_t)a->nslices * 32 + 255) / 256;
+    k_csr_to_sell<<<(unsigned)blocks, 256, 0, st>>>(a->view(), a->val, a->col, a->rp, nullptr,
+                                                    a->vstage, a->col_shift, a->nslices, 0);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(ctx, Status{PGM_ECUDA, cudaGetErrorString(e)});
+  return PGM_OK;
+}
+
+void pgm_matrix_destroy(pgm_matrix* a) {
+  if (!a) return;
+  dfree(a->sptr);
+  dfree(a->lane_len);
+  dfree(a->lane_row);
+  dfree(a->val);
+  dfree(a->col);
+  dfree(a->rp);
+  dfree(a->vstage);
+  delete a;
+}
+
+pgm_status pgm_matrix_info(const pgm_matrix* a, uint32_t* n, uint64_t* nnz, uint64_t* stored,
+                           uint64_t* device_bytes) {
+  if (!a) return PGM_EINVAL;
+  if (n) *n = a->n;
+  if (nnz) *nnz = a->nnz;
+  if (stored) *stored = a->stored;
+  if (device_bytes)
+    *device_bytes = a->stored * 12 + (uint64_t)a->nslices * (8 + 32 * 6) + 4ull * (a->n + 1) +
+                    8ull * a->nnz;
+  return PGM_OK;
+}
+
+pgm_status pgm_spmv(pgm_matrix* a, const double* x, double* y, int32_t flags) {
+  if (!a) return PGM_EINVAL;
+  pgm_context* ctx = a->ctx;
+  cudaSetDevice(ctx->device);
+  auto run = [&]() -> Status {
+    TRY(copy_in(ctx, ctx->tmp + ctx->lo, x, ctx->n, flags));
+    if (ctx->world > 1) TRY(halo_exchange(ctx, ctx->tmp));
+    TRY(set_gstate_idle(ctx));
+    Params P = make_params(ctx, ctx->dummy);
+    PlainEpi E{ctx->tmp, ctx->b + ctx->lo};
+    TRY(launch_spmv(ctx, a, P, E, 0));
+    TRY(copy_out(ctx, y, ctx->b + ctx->lo, ctx->n, flags));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return {};
+  };
+  Status s = run();
+  return s.code ? fail(ctx, s) : PGM_OK;
+}
+
+pgm_status pgm_deflator_create(pgm_context* ctx, const pgm_deflation_config* cfg,
+                               pgm_deflator** out) {
+  if (!ctx || !cfg || !out) return PGM_EINVAL;
+  if (cfg->r_max == 0) return fail(ctx, einval("deflation: r_max must be positive"));
+  if (cfg->drop == 0) return fail(ctx, einval("deflation: drop must be positive"));
+  if (cfg->r_max + 1 > (uint32_t)MAX_R1)
+    return fail(ctx, einval("deflation: r_max > " + std::to_string(MAX_R1 - 1) +
+                                " is not supported by the device path"));
+  cudaSetDevice(ctx->device);
+  auto* d = new pgm_deflator();
+  d->ctx = ctx;
+  d->cfg = *cfg;
+  d->R1 = (int)cfg->r_max + 1;
+  auto run = [&]() -> Status {
+    const int R1 = d->R1;
+    TRY(dalloc(&d->d, 1));
+    TRY(dalloc(&d->T, (size_t)R1 * R1));
+    TRY(dalloc(&d->Tinv, (size_t)R1 * R1));
+    TRY(dalloc(&d->Q, (size_t)R1 * R1));
+    TRY(dalloc(&d->proj, R1 + 1));
+    TRY(dalloc(&d->dwork, (size_t)16 * R1 * R1 + 32 * R1));
+    TRY(dalloc(&d->iwork, 4 * R1));
+    CU(cudaMemset(d->T, 0, 8 * R1 * R1));
+    CU(cudaMemset(d->Tinv, 0, 8 * R1 * R1));
+    DState ds{};
+    ds.r_max = (int)cfg->r_max;
+    ds.drop = (int)cfg->drop;
+    ds.accept_tol = cfg->accept_tol;
+    ds.inv_maxit = (int)cfg->inv_power_maxit;
+    ds.inv_tol = cfg->inv_power_tol;
+    ds.pow_maxit = (int)cfg->power_maxit;
+    CU(cudaMemcpy(d->d, &ds, sizeof(DState), cudaMemcpyHostToDevice));
+    TRY(defl_ensure_hist(d, 64));
+    return {};
+  };
+  Status s = run();
+  if (s.code) {
+    pgm_deflator_destroy(d);
+    return fail(ctx, s);
+  }
+  *out = d;
+  return PGM_OK;
+}
+
+void pgm_deflator_destroy(pgm_deflator* d) {
+  if (!d) return;
+  dfree(d->d);
+  dfree(d->U);
+  dfree(d->AU);
+  dfree(d->u);
+  dfree(d->T);
+  dfree(d->Tinv);
+  dfree(d->Q);
+  dfree(d->proj);
+  dfree(d->dwork);
+  dfree(d->iwork);
+  dfree(d->hist_restart);
+  dfree(d->hist_r);
+  dfree(d->hist_mu);
+  dfree(d->hist_theta);
+  delete d;
+}
+
+pgm_status pgm_deflator_reset(pgm_deflator* d) {
+  if (!d) return PGM_EINVAL;
+  DState ds;
+  cudaStreamSynchronize(d->ctx->stream);
+  cudaMemcpy(&ds, d->d, sizeof(DState), cudaMemcpyDeviceToHost);
+  ds.r = 0;
+  ds.mu = 0.0;
+  ds.skipped = 0;
+  ds.n_hist = 0;
+  ds.rotate = 0;
+  ds.push_ok = 0;
+  cudaError_t e = cudaMemcpy(d->d, &ds, sizeof(DState), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return fail(d->ctx, Status{PGM_ECUDA, cudaGetErrorString(e)});
+  return PGM_OK;
+}
+
+pgm_status pgm_deflator_info(pgm_deflator* d, uint32_t* rank, double* mu, uint32_t* skipped,
+                             uint32_t* n_history) {
+  if (!d) return PGM_EINVAL;
+  DState ds;
+  cudaStreamSynchronize(d->ctx->stream);
+  cudaError_t e = cudaMemcpy(&ds, d->d, sizeof(DState), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return fail(d->ctx, Status{PGM_ECUDA, cudaGetErrorString(e)});
+  if (rank) *rank = (uint32_t)ds.r;
+  if (mu) *mu = ds.mu;
+  if (skipped) *skipped = (uint32_t)ds.skipped;
+  if (n_history) *n_history = (uint32_t)ds.n_hist;
+  return PGM_OK;
+}
+
+pgm_status pgm_deflator_history(pgm_deflator* d, pgm_deflation_record* out, uint32_t cap) {
+  if (!d || !out) return PGM_EINVAL;
+  DState ds;
+  cudaStreamSynchronize(d->ctx->stream);
+  cudaMemcpy(&ds, d->d, sizeof(DState), cudaMemcpyDeviceToHost);
+  const uint32_t n = std::min<uint32_t>(cap, (uint32_t)std::min(ds.n_hist, d->hist_cap));
+  std::vector<uint32_t> hr(n), hrr(n);
+  std::vector<double> hm(n), ht(n);
+  if (n) {
+    cudaMemcpy(hr.data(), d->hist_restart, 4 * n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hrr.data(), d->hist_r, 4 * n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hm.data(), d->hist_mu, 8 * n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(ht.data(), d->hist_theta, 8 * n, cudaMemcpyDeviceToHost);
+  }
+  for (uint32_t i = 0; i < n; ++i) out[i] = {hr[i], hrr[i], hm[i], ht[i]};
+  return PGM_OK;
+}
+
+pgm_status pgm_deflator_basis(pgm_deflator* d, double* U, double* T) {
+  if (!d) return PGM_EINVAL;
+  pgm_context* ctx = d->ctx;
+  DState ds;
+  cudaStreamSynchronize(ctx->stream);
+  cudaMemcpy(&ds, d->d, sizeof(DState), cudaMemcpyDeviceToHost);
+  const int r = ds.r;
+  if (U && d->U)
+    for (int j = 0; j < r; ++j)
+      cudaMemcpy(U + (size_t)j * ctx->n, d->U + (size_t)j * ctx->ld + ctx->lo, 8 * ctx->n,
+                 cudaMemcpyDeviceToHost);
+  if (T && r > 0) {
+    std::vector<double> t((size_t)d->R1 * d->R1);
+    cudaMemcpy(t.data(), d->T, 8 * t.size(), cudaMemcpyDeviceToHost);
+    for (int j = 0; j < r; ++j)
+      for (int i = 0; i < r; ++i) T[i + j * r] = t[i + (size_t)j * d->R1];
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, Status{PGM_ECUDA, cudaGetErrorString(e)});
+  return PGM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void k_push_begin(DState* d, int R1) {
+  if (d->r >= R1) {
+    d->skipped++;
+    d->push_ok = 0;
+  } else {
+    d->push_ok = 1;
+  }
+  d->rotate = 0;
+}
+}  // namespace
+
+extern "C" {
+
+pgm_status pgm_deflator_push(pgm_deflator* d, pgm_matrix* a, const double* candidate,
+                             int32_t flags, int32_t* accepted) {
+  if (!d || !a || !candidate) return PGM_EINVAL;
+  pgm_context* ctx = d->ctx;
+  cudaSetDevice(ctx->device);
+  auto run = [&]() -> Status {
+    if (a->ctx != ctx) return einval("pgm_deflator_push: matrix from another context");
+    TRY(ensure_min_workspace(ctx, d->R1));
+    TRY(defl_alloc_vectors(d));
+    TRY(set_gstate_idle(ctx));
+    DState before;
+    CU(cudaMemcpy(&before, d->d, sizeof(DState), cudaMemcpyDeviceToHost));
+    TRY(copy_in(ctx, d->u + ctx->lo, candidate, ctx->n, flags));
+    const Params P = make_params(ctx, d);
+    const int R1 = d->R1;
+    k_push_begin<<<1, 1, 0, ctx->stream>>>(d->d, R1);
+    TRY(launch_sweep<SW_PUSH1>(ctx, P, 0, 0, 0, R1 + 1, false));
+    TRY(finish_global<SW_PUSH1>(ctx, P, 0, -1));
+    TRY(launch_sweep<SW_PUSH2>(ctx, P, 0, R1, 0, R1, true));
+    TRY(finish_global<SW_PUSH2>(ctx, P, 0, -1));
+    TRY(launch_sweep<SW_PUSH3>(ctx, P, 0, R1, 0, 1, false));
+    TRY(finish_global<SW_PUSH3>(ctx, P, 0, -1));
+    if (ctx->world > 1) TRY(halo_exchange(ctx, d->u));
+    TRY(launch_spmv(ctx, a, P, PushEpi{}, 2 * R1 + 1));
+    TRY(finish_global<102>(ctx, P, 0, -1));
+    k_rotate<false><<<ctx->nsm * 4, 256, 0, ctx->stream>>>(P);
+    k_clear_rotate<<<1, 1, 0, ctx->stream>>>(d->d);
+    CU(cudaGetLastError());
+    DState after;
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaMemcpy(&after, d->d, sizeof(DState), cudaMemcpyDeviceToHost));
+    if (accepted) *accepted = after.push_ok && (after.skipped == before.skipped);
+    return {};
+  };
+  Status s = run();
+  return s.code ? fail(ctx, s) : PGM_OK;
+}
+
+pgm_status pgm_deflator_truncate(pgm_deflator* d) {
+  if (!d) return PGM_EINVAL;
+  pgm_context* ctx = d->ctx;
+  cudaSetDevice(ctx->device);
+  auto run = [&]() -> Status {
+    TRY(ensure_min_workspace(ctx, d->R1));
+    TRY(defl_alloc_vectors(d));
+    const Params P = make_params(ctx, d);
+    k_truncate_once<<<1, 32, 0, ctx->stream>>>(P);
+    k_rotate<false><<<ctx->nsm * 4, 256, 0, ctx->stream>>>(P);
+    k_clear_rotate<<<1, 1, 0, ctx->stream>>>(d->d);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(ctx->stream));
+    return {};
+  };
+  Status s = run();
+  return s.code ? fail(ctx, s) : PGM_OK;
+}
+
+pgm_status pgm_deflator_observe_ritz(pgm_deflator* d, double value) {
+  if (!d) return PGM_EINVAL;
+  cudaSetDevice(d->ctx->device);
+  k_observe<<<1, 1, 0, d->ctx->stream>>>(d->d, value);
+  cudaError_t e = cudaStreamSynchronize(d->ctx->stream);
+  if (e != cudaSuccess) return fail(d->ctx, Status{PGM_ECUDA, cudaGetErrorString(e)});
+  return PGM_OK;
+}
+
+pgm_status pgm_deflator_apply(pgm_deflator* d, const double* v, double* w, int32_t flags) {
+  if (!d || !v || !w) return PGM_EINVAL;
+  pgm_context* ctx = d->ctx;
+  cudaSetDevice(ctx->device);
+  auto run = [&]() -> Status {
+    TRY(ensure_min_workspace(ctx, d->R1));
+    TRY(defl_alloc_vectors(d));
+    TRY(set_gstate_idle(ctx));
+    TRY(copy_in(ctx, d->u + ctx->lo, v, ctx->n, flags));
+    const Params P = make_params(ctx, d);
+    TRY(launch_sweep<SW_DOTS_U>(ctx, P, 0, 0, 0, d->R1, false));
+    TRY(finish_global<SW_DOTS_U>(ctx, P, 0, -1));
+    TRY(launch_sweep<SW_AXPY_U>(ctx, P, 0, d->R1, 0, 0, false));
+    TRY(copy_out(ctx, w, d->u + ctx->lo, ctx->n, flags));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return {};
+  };
+  Status s = run();
+  return s.code ? fail(ctx, s) : PGM_OK;
+}
+
+pgm_status pgm_solve(pgm_context* ctx, pgm_matrix* a, pgm_deflator* d, const double* b, double* x,
+                     const pgm_gmres_config* cfg, int32_t flags, pgm_report* rep) {
+  if (!ctx) return PGM_EINVAL;
+  cudaSetDevice(ctx->device);
+  Status s = solve_impl(ctx, a, d, b, x, cfg, flags, rep);
+  return s.code ? fail(ctx, s) : PGM_OK;
+}
+
+void pgm_report_free(pgm_report* rep) {
+  if (!rep) return;
+  std::free(rep->inner_restart);
+  std::free(rep->inner_step);
+  std::free(rep->inner_monitored);
+  std::free(rep->explicit_residual);
+  rep->inner_restart = rep->inner_step = nullptr;
+  rep->inner_monitored = rep->explicit_residual = nullptr;
+}
+
+}  // extern "C"

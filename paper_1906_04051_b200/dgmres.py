@@ -1,0 +1,489 @@
+"""Host-side mirror of the reference's solver API (include/dgmres/*.hpp) over the
+C ABI of libpgmres.so.  Same names, argument meaning and error behaviour:
+
+  reference (C++)                                  here
+  ---------------------------------------------    --------------------------------
+  GmresConfig        gmres.hpp:17-23               GmresConfig
+  GmresReport        gmres.hpp:31-44 (+write_csv)  GmresReport
+  DeflationConfig    deflation.hpp:15-22           DeflationConfig
+  Deflator           deflation.hpp:35-89           Deflator (state lives on the GPU)
+  Executor           parallel.hpp:86-128           DeviceExecutor (one GPU / one rank)
+  CsrMatrix          sparse.hpp:17-24              CsrMatrix (host) / DeviceCsr (resident)
+  deflated_gmres     deflation.hpp:97-98           deflated_gmres
+  gmres_restarted    gmres.hpp:110-113             gmres_restarted (opA = CSR, opM = None)
+
+std::invalid_argument -> ValueError, std::runtime_error -> GmresError (a
+RuntimeError).  Arrays may be numpy (host) or torch CUDA tensors (device
+resident, no copies).  There is no CPU fallback: without the CUDA library
+every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import io
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi as capi
+
+
+class GmresError(RuntimeError):
+    """std::runtime_error of gmres.cpp (non-finite values, singular projection)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA / NCCL / allocation failure."""
+
+
+def _raise(code: int, msg: str):
+    if code == capi.PGM_EINVAL:
+        raise ValueError(msg)
+    if code in (capi.PGM_ENONFINITE, capi.PGM_ESINGULAR):
+        raise GmresError(msg)
+    raise DeviceError(f"pgmres error {code}: {msg}")
+
+
+def _check(code: int, ctx=None):
+    if code != capi.PGM_OK:
+        L = capi.lib()
+        _raise(code, L.pgm_last_error(ctx).decode(errors="replace"))
+
+
+def _is_cuda(a) -> bool:
+    return hasattr(a, "is_cuda") and bool(a.is_cuda)
+
+
+def _ptr(a, dtype):
+    """(pointer, flags, keepalive) for a numpy array or a torch CUDA tensor."""
+    if _is_cuda(a):
+        import torch
+
+        want = torch.float64 if dtype == np.float64 else torch.int32
+        if a.dtype not in (want, torch.uint32 if want == torch.int32 else want):
+            raise ValueError(f"device array must be {want}")
+        if not a.is_contiguous():
+            raise ValueError("device array must be contiguous")
+        return a.data_ptr(), capi.PGM_DEVICE_PTRS, a
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return arr.ctypes.data, 0, arr
+
+
+@dataclass
+class GmresConfig:
+    m: int = 50
+    max_restarts: int = 100
+    rel_tol: float = 1e-8
+    fixed_iterations: bool = False
+    breakdown_scale: float = 1e-14
+
+    def _c(self):
+        if self.m < 0 or self.max_restarts < 0:
+            raise ValueError("GmresConfig: negative size")
+        return capi.GmresConfigC(int(self.m), int(self.max_restarts), float(self.rel_tol),
+                                 int(bool(self.fixed_iterations)), float(self.breakdown_scale))
+
+
+@dataclass
+class DeflationConfig:
+    r_max: int = 20
+    drop: int = 1
+    accept_tol: float = 1e-8
+    inv_power_maxit: int = 500
+    inv_power_tol: float = 1e-10
+    power_maxit: int = 200
+
+    def _c(self):
+        return capi.DeflationConfigC(int(self.r_max), int(self.drop), float(self.accept_tol),
+                                     int(self.inv_power_maxit), float(self.inv_power_tol),
+                                     int(self.power_maxit))
+
+
+@dataclass
+class InnerRecord:
+    restart: int
+    inner: int
+    monitored: float
+
+
+@dataclass
+class DeflationRecord:
+    restart: int
+    r: int
+    mu: float
+    smallest_ritz: float
+
+
+@dataclass
+class GmresReport:
+    beta0: float = 0.0
+    inner_restart: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+    inner_step: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+    monitored: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    explicit_residual: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    restarts: int = 0
+    total_inner: int = 0
+    converged: bool = False
+    breakdown: bool = False
+    final_relative: float = 0.0
+    solve_seconds: float = 0.0  # device time (CUDA events) of the whole solve
+
+    @property
+    def inner(self):
+        return [InnerRecord(int(r), int(k), float(mv)) for r, k, mv in
+                zip(self.inner_restart, self.inner_step, self.monitored)]
+
+    def write_csv(self, os_=None) -> str:
+        """restart,inner_step,monitored_residual,explicit_residual (gmres.cpp:117-130)."""
+        out = io.StringIO()
+        out.write("restart,inner_step,monitored_residual,explicit_residual\n")
+        n = len(self.monitored)
+        for i in range(n):
+            r = int(self.inner_restart[i])
+            closes = i + 1 == n or int(self.inner_restart[i + 1]) != r
+            out.write(f"{r},{int(self.inner_step[i])},{_g17(self.monitored[i])},")
+            if closes and r < len(self.explicit_residual):
+                out.write(_g17(self.explicit_residual[r]))
+            out.write("\n")
+        s = out.getvalue()
+        if os_ is not None:
+            os_.write(s)
+        return s
+
+
+def _g17(v: float) -> str:
+    """std::ostream with precision(17) (default float format = %.17g)."""
+    return format(float(v), ".17g")
+
+
+@dataclass
+class CsrMatrix:
+    """Host CSR (sparse.hpp:17-24): uint32 row_ptr/col_idx, fp64 values."""
+    n: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(len(self.col_idx))
+
+
+class DeviceExecutor:
+    """One GPU (one rank of a z-slab partition when world > 1).
+
+    Mirrors the role of dgmres::Executor: owns the device resources and the
+    partition; kernels are issued through it.  Single-GPU contexts are created
+    lazily from the first matrix's size."""
+
+    def __init__(self, device: int = 0, *, n_global: int | None = None, n_axis: int = 0,
+                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+        self.device, self.rank, self.world = device, rank, world
+        self.n_axis = n_axis
+        self._nccl_id = nccl_id
+        self._ctx = None
+        self.n_global = n_global
+        if n_global is not None:
+            self._create(n_global)
+
+    def _create(self, n_global: int):
+        L = capi.lib()
+        idbuf = None
+        if self.world > 1:
+            if self._nccl_id is None or len(self._nccl_id) != 128:
+                raise ValueError("world > 1 needs a 128-byte ncclUniqueId")
+            idbuf = C.create_string_buffer(bytes(self._nccl_id), 128)
+        cfg = capi.ContextConfig(self.device, self.rank, self.world,
+                                 C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
+                                 self.n_axis, int(n_global), 1)
+        h = C.c_void_p()
+        _check(L.pgm_context_create(C.byref(cfg), C.byref(h)))
+        self._ctx = h
+        self.n_global = int(n_global)
+
+    def _ensure(self, n_global: int):
+        if self._ctx is None:
+            self._create(n_global)
+        elif n_global != self.n_global:
+            raise ValueError(f"executor was built for n={self.n_global}, got n={n_global}")
+
+    @property
+    def handle(self):
+        if self._ctx is None:
+            raise ValueError("executor not initialised (no matrix seen yet)")
+        return self._ctx
+
+    def partition(self):
+        p = capi.Partition()
+        _check(capi.lib().pgm_context_partition(self.handle, C.byref(p)), self.handle)
+        return dict(row_begin=p.row_begin, row_end=p.row_end, halo_lo=p.halo_lo,
+                    halo_hi=p.halo_hi)
+
+    @property
+    def n_own(self) -> int:
+        p = self.partition()
+        return p["row_end"] - p["row_begin"]
+
+    def stream(self) -> int:
+        return int(capi.lib().pgm_context_stream(self.handle) or 0)
+
+    def launch_count(self) -> int:
+        return int(capi.lib().pgm_context_launch_count(self.handle))
+
+    def upload(self, A: CsrMatrix) -> "DeviceCsr":
+        return DeviceCsr(self, A)
+
+    def spmv(self, A, x, y=None):
+        """Executor::spmv (parallel.hpp:93)."""
+        dA = A if isinstance(A, DeviceCsr) else DeviceCsr(self, A)
+        n = self.n_own
+        if y is None:
+            y = np.empty(n) if not _is_cuda(x) else x.new_empty(n)
+        xp, f1, _kx = _ptr(x, np.float64)
+        yp, f2, _ky = _ptr(y, np.float64)
+        if f1 != f2:
+            raise ValueError("x and y must both be host or both be device arrays")
+        _check(capi.lib().pgm_spmv(dA.handle, xp, yp, f1), self.handle)
+        return y
+
+    def close(self):
+        if self._ctx is not None:
+            capi.lib().pgm_context_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceCsr:
+    """A CSR matrix resident on the executor's GPU (SELL-32 layout)."""
+
+    def __init__(self, ex: DeviceExecutor, A: CsrMatrix, *, n_global: int | None = None):
+        ex._ensure(n_global if n_global is not None else A.n if ex.world == 1 else ex.n_global)
+        self.ex = ex
+        self.n = int(A.n)
+        self.nnz = A.nnz
+        rp, f1, k1 = _ptr(A.row_ptr, np.uint32)
+        ci, f2, k2 = _ptr(A.col_idx, np.uint32)
+        va, f3, k3 = _ptr(A.values, np.float64)
+        if not (f1 == f2 == f3):
+            raise ValueError("CSR arrays must all be host or all be device arrays")
+        view = capi.CsrView(self.n, self.nnz, rp, ci, va)
+        h = C.c_void_p()
+        _check(capi.lib().pgm_matrix_upload(ex.handle, C.byref(view), f1, C.byref(h)), ex.handle)
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def update_values(self, values):
+        vp, f, _k = _ptr(values, np.float64)
+        _check(capi.lib().pgm_matrix_update_values(self._h, vp, f), self.ex.handle)
+
+    def info(self):
+        n, nnz, st, by = C.c_uint32(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(capi.lib().pgm_matrix_info(self._h, C.byref(n), C.byref(nnz), C.byref(st),
+                                          C.byref(by)))
+        return dict(n=n.value, nnz=nnz.value, stored=st.value, device_bytes=by.value)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            capi.lib().pgm_matrix_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Deflator:
+    """Deflation preconditioner M^{-1} = I + U(|mu|T^{-1} - I)U^T (deflation.hpp:35-89).
+
+    U, AU, T, T^{-1} and the running mu live on the GPU of the executor the
+    deflator is first used with."""
+
+    def __init__(self, cfg: DeflationConfig | None = None, ex: DeviceExecutor | None = None):
+        self.cfg = cfg or DeflationConfig()
+        if self.cfg.r_max == 0:
+            raise ValueError("deflation: r_max must be positive")
+        if self.cfg.drop == 0:
+            raise ValueError("deflation: drop must be positive")
+        self._h = None
+        self.ex = None
+        if ex is not None and ex._ctx is not None:
+            self._bind(ex)
+
+    def _bind(self, ex: DeviceExecutor):
+        if self._h is not None:
+            if ex is not self.ex:
+                raise ValueError("deflator is bound to another executor")
+            return
+        h = C.c_void_p()
+        c = self.cfg._c()
+        _check(capi.lib().pgm_deflator_create(ex.handle, C.byref(c), C.byref(h)), ex.handle)
+        self._h, self.ex = h, ex
+
+    def _info(self):
+        if self._h is None:
+            return 0, 0.0, 0, 0
+        r, mu, sk, nh = C.c_uint32(), C.c_double(), C.c_uint32(), C.c_uint32()
+        _check(capi.lib().pgm_deflator_info(self._h, C.byref(r), C.byref(mu), C.byref(sk),
+                                            C.byref(nh)), self.ex.handle)
+        return r.value, mu.value, sk.value, nh.value
+
+    def rank(self) -> int:
+        return self._info()[0]
+
+    def mu(self) -> float:
+        return self._info()[1]
+
+    def skipped_updates(self) -> int:
+        return self._info()[2]
+
+    def reset(self):
+        if self._h is not None:
+            _check(capi.lib().pgm_deflator_reset(self._h), self.ex.handle)
+
+    def history(self):
+        nh = self._info()[3]
+        if nh == 0:
+            return []
+        recs = (capi.DeflationRecordC * nh)()
+        _check(capi.lib().pgm_deflator_history(self._h, recs, nh), self.ex.handle)
+        return [DeflationRecord(r.restart, r.r, r.mu, r.smallest_ritz) for r in recs]
+
+    def write_csv(self, os_=None) -> str:
+        """restart,r,mu,smallest_ritz (deflation.cpp:266-273)."""
+        s = "restart,r,mu,smallest_ritz\n" + "".join(
+            f"{h.restart},{h.r},{_g17(h.mu)},{_g17(h.smallest_ritz)}\n" for h in self.history())
+        if os_ is not None:
+            os_.write(s)
+        return s
+
+    def T_block(self) -> np.ndarray:
+        r = self.rank()
+        if r == 0:
+            return np.zeros((0, 0))
+        T = np.zeros(r * r)
+        _check(capi.lib().pgm_deflator_basis(self._h, None, T.ctypes.data), self.ex.handle)
+        return T.reshape(r, r, order="F")
+
+    def basis_matrix(self) -> np.ndarray:
+        """Active columns of U (n_own x rank)."""
+        r = self.rank()
+        n = self.ex.n_own if self.ex is not None else 0
+        U = np.zeros(max(1, n * r))
+        if r:
+            _check(capi.lib().pgm_deflator_basis(self._h, U.ctypes.data, None), self.ex.handle)
+        return U[: n * r].reshape(r, n).T
+
+    def observe_ritz(self, value: float):
+        self._need()
+        _check(capi.lib().pgm_deflator_observe_ritz(self._h, float(value)), self.ex.handle)
+
+    def truncate(self):
+        self._need()
+        _check(capi.lib().pgm_deflator_truncate(self._h), self.ex.handle)
+
+    def push_vector(self, candidate, A, ex: DeviceExecutor | None = None) -> bool:
+        """push_vector(candidate, opA = spmv(A)) (deflation.cpp:123-184)."""
+        ex = ex or self.ex or DeviceExecutor()
+        dA = A if isinstance(A, DeviceCsr) else DeviceCsr(ex, A)
+        self._bind(ex)
+        cp, f, _k = _ptr(candidate, np.float64)
+        acc = C.c_int32()
+        _check(capi.lib().pgm_deflator_push(self._h, dA.handle, cp, f, C.byref(acc)), ex.handle)
+        return bool(acc.value)
+
+    def apply(self, v, ex: DeviceExecutor | None = None):
+        """w = v + U(|mu| T^{-1} - I) U^T v (deflation.cpp:104-117)."""
+        if self._h is None:
+            return np.array(v, dtype=np.float64, copy=True) if not _is_cuda(v) else v.clone()
+        vp, f, _k = _ptr(v, np.float64)
+        w = np.empty(self.ex.n_own) if not f else v.new_empty(self.ex.n_own)
+        wp, f2, _k2 = _ptr(w, np.float64)
+        _check(capi.lib().pgm_deflator_apply(self._h, vp, wp, f), self.ex.handle)
+        return w
+
+    def _need(self):
+        if self._h is None:
+            raise ValueError("deflator has no basis yet (never used with an executor)")
+
+    def close(self):
+        if self._h is not None:
+            capi.lib().pgm_deflator_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _solve(A, b, x, cfg: GmresConfig, d: Deflator | None, ex: DeviceExecutor) -> GmresReport:
+    if cfg.m == 0:
+        raise ValueError("GmresWorkspace: m must be positive")
+    dA = A if isinstance(A, DeviceCsr) else DeviceCsr(ex, A)
+    if d is not None:
+        d._bind(ex)
+    bp, f1, _kb = _ptr(b, np.float64)
+    if _is_cuda(x):
+        xp, f2, _kx = x.data_ptr(), capi.PGM_DEVICE_PTRS, x
+        host_x = None
+    else:
+        if not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags.c_contiguous):
+            raise ValueError("x must be a contiguous float64 numpy array (updated in place)")
+        xp, f2, host_x = x.ctypes.data, 0, x
+    if f1 != f2:
+        raise ValueError("b and x must both be host or both be device arrays")
+    rep = capi.ReportC()
+    c = cfg._c()
+    L = capi.lib()
+    code = L.pgm_solve(ex.handle, dA.handle, d._h if d is not None else None, bp, xp,
+                       C.byref(c), f1, C.byref(rep))
+    _check(code, ex.handle)
+    del host_x
+    try:
+        ni, nr = rep.n_inner, rep.restarts
+        out = GmresReport(
+            beta0=rep.beta0,
+            inner_restart=np.ctypeslib.as_array(rep.inner_restart, (max(ni, 1),))[:ni].copy(),
+            inner_step=np.ctypeslib.as_array(rep.inner_step, (max(ni, 1),))[:ni].copy(),
+            monitored=np.ctypeslib.as_array(rep.inner_monitored, (max(ni, 1),))[:ni].copy(),
+            explicit_residual=np.ctypeslib.as_array(rep.explicit_residual,
+                                                    (max(nr, 1),))[:nr].copy(),
+            restarts=rep.restarts, total_inner=int(rep.total_inner),
+            converged=bool(rep.converged), breakdown=bool(rep.breakdown),
+            final_relative=rep.final_relative, solve_seconds=rep.solve_seconds)
+    finally:
+        L.pgm_report_free(C.byref(rep))
+    return out
+
+
+def deflated_gmres(A, b, x, cfg: GmresConfig, d: Deflator, ex: DeviceExecutor) -> GmresReport:
+    """deflation.hpp:97-98.  x: initial guess in, iterate out (in place)."""
+    if d is None:
+        raise ValueError("deflated_gmres needs a Deflator")
+    return _solve(A, b, x, cfg, d, ex)
+
+
+def gmres_restarted(opA, opM, b, x, cfg: GmresConfig, ex: DeviceExecutor,
+                    hook=None) -> GmresReport:
+    """gmres.hpp:110-113 for the production operator pair (opA = CSR SpMV,
+    opM = nullptr).  Arbitrary std::function operators and hooks stay on the
+    reference; the device path accepts only matrices (no CPU fallback)."""
+    if opM is not None:
+        raise ValueError("gmres_restarted: the device path takes opM=None; "
+                         "use deflated_gmres for the deflation preconditioner")
+    if hook is not None:
+        raise ValueError("gmres_restarted: restart hooks are not supported on the device path")
+    if not isinstance(opA, (CsrMatrix, DeviceCsr)):
+        raise ValueError("gmres_restarted: opA must be a CsrMatrix or DeviceCsr")
+    return _solve(opA, b, x, cfg, None, ex)

@@ -1,0 +1,416 @@
+"""GPU parity: libpgmres (through the C ABI) against the reference.
+
+Tolerances (north star): same iteration count +-1, residual
+history within 1e-10 * beta0, solution within 1e-8 relative; SpMV bit-exact
+(ascending-column accumulation, no FMA contraction, sparse.cpp:9-19)."""
+import numpy as np
+import pytest
+
+import paper_1906_04051_b200 as pg
+
+pytestmark = pytest.mark.gpu
+
+HIST_TOL = 1e-10  # relative to beta0
+X_TOL = 1e-8
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _csr(R, ne):
+    A, b = R.first_newton_system(ne)
+    return pg.CsrMatrix(A.n, A.row_ptr, A.col_idx, A.values), A, b
+
+
+def _compare(rep, g, x, x_ref=None, total_tol=1):
+    b0 = float(g["beta0"])
+    assert rep.beta0 == pytest.approx(b0, rel=1e-12)
+    assert abs(rep.total_inner - int(g["total_inner"])) <= total_tol
+    n = min(len(rep.monitored), len(g["monitored"]))
+    assert np.max(np.abs(rep.monitored[:n] - g["monitored"][:n])) <= HIST_TOL * b0
+    k = min(len(rep.explicit_residual), len(g["explicit_residual"]))
+    assert np.max(np.abs(rep.explicit_residual[:k] - g["explicit_residual"][:k])) <= HIST_TOL * b0
+    if x_ref is not None:
+        assert np.linalg.norm(x - x_ref) <= X_TOL * np.linalg.norm(x_ref)
+
+
+# ---------------------------------------------------------------------------
+# SpMV (sparse.cpp:9-19, Executor::spmv parallel.cpp:230-277)
+
+def test_spmv_bitexact_bratu(torch_cuda, ref):
+    for ne in (1, 2, 5, 10):
+        A, Ar, _ = _csr(ref, ne)
+        ex = pg.DeviceExecutor()
+        x = np.random.default_rng(ne).uniform(-1, 1, A.n)
+        y = ex.spmv(A, x)
+        assert np.array_equal(y, ref.spmv(Ar, x)), ne
+
+
+def test_spmv_bitexact_irregular(torch_cuda, ref):
+    # empty rows, a dense row, long and short rows, unsorted-by-length tiles
+    rng = np.random.default_rng(5)
+    n = 3000
+    lens = rng.integers(0, 40, n)
+    lens[7] = 0
+    lens[100] = n
+    lens[2000:2600] = 1
+    rp = np.zeros(n + 1, np.uint32)
+    rp[1:] = np.cumsum(lens)
+    ci = np.concatenate([np.sort(rng.choice(n, size=l, replace=False)) for l in lens]).astype(np.uint32)
+    va = rng.standard_normal(rp[-1])
+    A = pg.CsrMatrix(n, rp, ci, va)
+    x = rng.standard_normal(n)
+    ex = pg.DeviceExecutor()
+    from oracle.refbind import Csr
+    assert np.array_equal(ex.spmv(A, x), ref.spmv(Csr(n, rp, ci, va), x))
+
+
+def test_spmv_device_pointers(torch_cuda, ref):
+    torch = torch_cuda
+    A, Ar, _ = _csr(ref, 4)
+    ex = pg.DeviceExecutor()
+    dA = ex.upload(A)
+    x = np.random.default_rng(3).uniform(-1, 1, A.n)
+    y = ex.spmv(dA, torch.tensor(x, device="cuda"))
+    assert np.array_equal(y.cpu().numpy(), ref.spmv(Ar, x))
+    # update_values (Newton reuses the pattern, assembly.cpp:253)
+    dA.update_values(2.0 * A.values)
+    assert np.array_equal(ex.spmv(dA, x), 2.0 * ref.spmv(Ar, x))
+
+
+# ---------------------------------------------------------------------------
+# The hot path: deflated_gmres / gmres_restarted
+
+def test_cfg1_deflated(torch_cuda, ref, golden):
+    A, _, b = _csr(ref, 10)
+    g = golden("cfg1_defl")
+    ex = pg.DeviceExecutor()
+    d = pg.Deflator()
+    x = np.zeros(A.n)
+    rep = pg.deflated_gmres(A, b, x, pg.GmresConfig(m=30, rel_tol=1e-10), d, ex)
+    assert rep.converged and not rep.breakdown
+    assert rep.restarts == int(g["restarts"])
+    _compare(rep, g, x, g["x"])
+    assert d.rank() == int(g["rank"])
+    assert d.mu() == pytest.approx(float(g["mu"]), rel=1e-8)
+    h = d.history()
+    assert [r.r for r in h] == list(g["hist_r"])
+    assert np.allclose([r.smallest_ritz for r in h], g["hist_theta"], rtol=1e-7)
+    assert np.abs(d.T_block() - g["T"]).max() <= 1e-8 * np.abs(g["T"]).max()
+
+
+def test_cfg1_plain(torch_cuda, ref, golden):
+    A, _, b = _csr(ref, 10)
+    g = golden("cfg1_plain")
+    ex = pg.DeviceExecutor()
+    x = np.zeros(A.n)
+    rep = pg.gmres_restarted(A, None, b, x, pg.GmresConfig(m=30, rel_tol=1e-10), ex)
+    assert rep.converged and rep.restarts == int(g["restarts"])
+    _compare(rep, g, x, g["x"])
+
+
+def test_truncation_run_matches_reference(torch_cuda, ref, golden):
+    A, _, b = _csr(ref, 10)
+    g = golden("ne10_m4_trunc")
+    ex = pg.DeviceExecutor()
+    d = pg.Deflator()
+    x = np.zeros(A.n)
+    rep = pg.deflated_gmres(A, b, x, pg.GmresConfig(m=4, max_restarts=24, fixed_iterations=True),
+                            d, ex)
+    assert rep.restarts == 24 and rep.total_inner == 96 and not rep.converged
+    _compare(rep, g, x, g["x"], total_tol=0)
+    assert [r.r for r in d.history()] == list(g["hist_r"])
+    assert np.abs(d.T_block() - g["T"]).max() <= 1e-8 * np.abs(g["T"]).max()
+    U = d.basis_matrix()
+    assert np.abs(U.T @ U - np.eye(d.rank())).max() < 1e-10
+    AU = np.stack([ex.spmv(A, U[:, j]) for j in range(d.rank())], axis=1)
+    T = d.T_block()
+    assert np.abs(T - U.T @ AU).max() < 1e-10 * np.abs(T).max()
+
+
+def test_fixed_run_to_rounding_floor(torch_cuda, ref, golden):
+    A, _, b = _csr(ref, 4)
+    g = golden("ne4_fixed_trunc")
+    ex = pg.DeviceExecutor()
+    d = pg.Deflator()
+    x = np.zeros(A.n)
+    rep = pg.deflated_gmres(A, b, x, pg.GmresConfig(m=10, max_restarts=26, fixed_iterations=True),
+                            d, ex)
+    assert rep.restarts == 26 and rep.total_inner == 260
+    b0 = float(g["beta0"])
+    assert np.max(np.abs(rep.explicit_residual - g["explicit_residual"])) <= HIST_TOL * b0
+    assert d.rank() <= 20
+    assert np.linalg.norm(x - g["x"]) <= X_TOL * np.linalg.norm(g["x"])
+
+
+def test_dense_lu_equivalence(torch_cuda, golden):
+    # criterion 4 (acceptance.cpp:214-261): n_e = 2, plain and deflated vs dense LU
+    s = golden("ne2_system")
+    n = s["rhs"].size
+    A = pg.CsrMatrix(n, s["row_ptr"], s["col_idx"], s["values"])
+    dense = np.zeros((n, n))
+    for i in range(n):
+        for k in range(s["row_ptr"][i], s["row_ptr"][i + 1]):
+            dense[i, s["col_idx"][k]] = s["values"][k]
+    xd = np.linalg.solve(dense, s["rhs"])
+    ex = pg.DeviceExecutor()
+    cfg = pg.GmresConfig(m=50, max_restarts=100, rel_tol=1e-12)
+    x1 = np.zeros(n)
+    pg.gmres_restarted(A, None, s["rhs"], x1, cfg, ex)
+    x2 = np.zeros(n)
+    pg.deflated_gmres(A, s["rhs"], x2, cfg, pg.Deflator(pg.DeflationConfig(r_max=20)), ex)
+    assert np.linalg.norm(x1 - xd) <= 1e-10 * np.linalg.norm(xd)
+    assert np.linalg.norm(x2 - xd) <= 1e-10 * np.linalg.norm(xd)
+
+
+def test_finite_termination(torch_cuda, golden):
+    # test_gmres.cpp:232-254: m = 125 >= 45 free DOF, one restart, exhausts the space
+    s = golden("ne2_system")
+    n = s["rhs"].size
+    A = pg.CsrMatrix(n, s["row_ptr"], s["col_idx"], s["values"])
+    ex = pg.DeviceExecutor()
+    x = np.zeros(n)
+    rep = pg.gmres_restarted(A, None, s["rhs"], x,
+                             pg.GmresConfig(m=125, max_restarts=1, rel_tol=1e-12), ex)
+    assert rep.converged and rep.total_inner <= 125
+
+
+def test_crit10_spectral_action(torch_cuda, golden):
+    # acceptance.cpp:539-595 on diag(1..50)
+    g = golden("crit10_diag")
+    n = 50
+    A = pg.CsrMatrix(n, np.arange(n + 1, dtype=np.uint32), np.arange(n, dtype=np.uint32),
+                     np.arange(1, n + 1, dtype=np.float64))
+    ex = pg.DeviceExecutor()
+    d = pg.Deflator(pg.DeflationConfig(r_max=20))
+    x = np.zeros(n)
+    pg.deflated_gmres(A, np.full(n, 1 / np.sqrt(n)), x,
+                      pg.GmresConfig(m=8, max_restarts=5, fixed_iterations=True), d, ex)
+    assert d.rank() == 5 and d.mu() == pytest.approx(float(g["mu"]), rel=1e-9)
+    bm = np.zeros((n, n))
+    for j in range(n):
+        e = np.zeros(n)
+        e[j] = 1.0
+        bm[:, j] = np.arange(1, n + 1) * d.apply(e)
+    ev = np.linalg.eigvals(bm)
+    mu = d.mu()
+    assert np.sum(np.abs(ev.real - mu) / mu < 0.05) >= 5
+    assert ev.real.min() > 5.5 and np.abs(ev.imag).max() < 1e-8
+    assert np.linalg.norm(x - g["x"]) <= 1e-10 * np.linalg.norm(g["x"])
+
+
+def test_crit3_midflight(torch_cuda, ref, golden):
+    A, _, b = _csr(ref, 25)
+    g = golden("crit3_ne25")
+    ex = pg.DeviceExecutor()
+    cfg = pg.GmresConfig(m=50, max_restarts=3, fixed_iterations=True)
+    x = np.zeros(A.n)
+    rd = pg.deflated_gmres(A, b, x, cfg, pg.Deflator(), ex)
+    x2 = np.zeros(A.n)
+    rp = pg.gmres_restarted(A, None, b, x2, cfg, ex)
+    b0 = float(g["beta0"])
+    assert np.max(np.abs(rd.explicit_residual - g["defl_explicit"])) <= HIST_TOL * b0
+    assert np.max(np.abs(rp.explicit_residual - g["plain_explicit"])) <= HIST_TOL * b0
+    assert np.max(np.abs(rd.monitored - g["defl_monitored"])) <= HIST_TOL * b0
+
+
+@pytest.mark.slow
+def test_cfg2_deflated(torch_cuda, ref, golden):
+    """BASELINE config 2: n_e = 50 (1,030,301 DOF), GMRES(50) + deflation, tol 1e-10."""
+    A, _, b = _csr(ref, 50)
+    g = golden("cfg2_defl")
+    ex = pg.DeviceExecutor()
+    d = pg.Deflator()
+    x = np.zeros(A.n)
+    rep = pg.deflated_gmres(A, b, x, pg.GmresConfig(m=50, rel_tol=1e-10), d, ex)
+    assert rep.converged
+    assert abs(rep.restarts - int(g["restarts"])) <= 1
+    _compare(rep, g, x)
+    assert abs(np.linalg.norm(x) - float(g["x_norm"])) <= X_TOL * float(g["x_norm"])
+    assert np.linalg.norm(x[::997] - g["x_sample"]) <= X_TOL * np.linalg.norm(g["x_sample"]) * 10
+    assert d.rank() == int(g["rank"])
+
+
+# ---------------------------------------------------------------------------
+# Unit-level ports of test_gmres.cpp / test_deflation.cpp
+
+def _diag(vals):
+    n = len(vals)
+    return pg.CsrMatrix(n, np.arange(n + 1, dtype=np.uint32), np.arange(n, dtype=np.uint32),
+                        np.asarray(vals, np.float64))
+
+
+def test_identity_converges_at_first_step(torch_cuda):
+    ex = pg.DeviceExecutor()
+    b = np.array([1.0, -2.0, 3.0, 0.5, -0.25])
+    x = np.zeros(5)
+    rep = pg.gmres_restarted(_diag(np.ones(5)), None, b, x, pg.GmresConfig(m=5), ex)
+    assert rep.converged and rep.breakdown and rep.total_inner == 1
+    assert abs(rep.monitored[0]) < 1e-14
+    assert np.allclose(x, b, atol=1e-14)
+
+
+def test_scaled_identity_and_eigenvector_start(torch_cuda):
+    ex = pg.DeviceExecutor()
+    x = np.zeros(3)
+    rep = pg.gmres_restarted(_diag([2.0, 2.0, 2.0]), None, np.array([4.0, 0, 0]), x,
+                             pg.GmresConfig(), ex)
+    assert rep.converged and abs(x[0] - 2.0) < 1e-15 and np.abs(x[1:]).max() < 1e-15
+    ex2 = pg.DeviceExecutor()
+    x = np.zeros(3)
+    rep = pg.gmres_restarted(_diag([1.0, 2.0, 3.0]), None, np.array([1.0, 0, 0]), x,
+                             pg.GmresConfig(), ex2)
+    assert rep.breakdown and rep.converged and rep.total_inner == 1 and abs(x[0] - 1) < 1e-15
+
+
+def test_plane_rotation(torch_cuda):
+    # test_gmres.cpp:108-137: A = [[0,-1],[1,0]], b = e1 -> x = (0, -1)
+    A = pg.CsrMatrix(2, np.array([0, 1, 2], np.uint32), np.array([1, 0], np.uint32),
+                     np.array([-1.0, 1.0]))
+    ex = pg.DeviceExecutor()
+    x = np.zeros(2)
+    rep = pg.gmres_restarted(A, None, np.array([1.0, 0.0]), x, pg.GmresConfig(m=2), ex)
+    assert rep.monitored[0] == 1.0 and rep.monitored[1] == 0.0
+    assert np.allclose(x, [0.0, -1.0], atol=1e-15)
+
+
+def test_zero_rhs_and_errors(torch_cuda):
+    ex = pg.DeviceExecutor()
+    x = np.zeros(4)
+    rep = pg.gmres_restarted(_diag(np.ones(4)), None, np.zeros(4), x, pg.GmresConfig(), ex)
+    assert rep.converged and rep.total_inner == 0 and rep.restarts == 0
+    with pytest.raises(ValueError):
+        pg.gmres_restarted(_diag(np.ones(4)), None, np.ones(4), x, pg.GmresConfig(m=0), ex)
+    bad = _diag([np.nan, 1.0])
+    ex2 = pg.DeviceExecutor()
+    with pytest.raises(pg.GmresError):
+        pg.gmres_restarted(bad, None, np.ones(2), np.zeros(2), pg.GmresConfig(), ex2)
+    with pytest.raises(ValueError):
+        pg.Deflator(pg.DeflationConfig(r_max=0))
+    with pytest.raises(ValueError):
+        pg.Deflator(pg.DeflationConfig(r_max=5, drop=0))
+
+
+def test_fixed_iteration_mode(torch_cuda):
+    rng = np.random.default_rng(61)
+    n = 8
+    r = rng.standard_normal((n, n))
+    a = r.T @ r + n * np.eye(n)
+    rp = np.arange(0, n * n + 1, n, dtype=np.uint32)
+    ci = np.tile(np.arange(n, dtype=np.uint32), n)
+    A = pg.CsrMatrix(n, rp, ci, a.ravel())
+    ex = pg.DeviceExecutor()
+    x = np.zeros(n)
+    rep = pg.gmres_restarted(A, None, rng.standard_normal(n), x,
+                             pg.GmresConfig(m=2, max_restarts=7, fixed_iterations=True,
+                                            rel_tol=1e-1), ex)
+    assert rep.restarts == 7 and len(rep.explicit_residual) == 7 and rep.total_inner == 14
+    assert not rep.converged
+
+
+def test_deflator_truncation_exact(torch_cuda):
+    # test_deflation.cpp:55-75
+    ex = pg.DeviceExecutor()
+    A = _diag([1.0, 2.0, 3.0])
+    d = pg.Deflator()
+    for i in range(3):
+        e = np.zeros(3)
+        e[i] = 1.0
+        assert d.push_vector(e, A, ex)
+    assert d.rank() == 3
+    d.truncate()
+    assert d.rank() == 2
+    T = d.T_block()
+    assert np.allclose(T, np.diag([1.0, 2.0]), atol=1e-14)
+    U = d.basis_matrix()
+    assert np.abs(U[2, :]).max() < 1e-14
+
+
+def test_deflator_cap_and_span(torch_cuda):
+    # test_deflation.cpp:77-104
+    ex = pg.DeviceExecutor()
+    A = _diag([1.0, 2.0, 3.0, 4.0, 5.0])
+    d = pg.Deflator(pg.DeflationConfig(r_max=3))
+    for i in range(4):
+        e = np.zeros(5)
+        e[i] = 1.0
+        assert d.push_vector(e, A, ex)
+    assert d.rank() == 3
+    assert np.allclose(np.diag(d.T_block()), [1.0, 2.0, 3.0], atol=1e-12)
+    ex2 = pg.DeviceExecutor()
+    A3 = _diag([1.0, 2.0, 3.0])
+    d2 = pg.Deflator()
+    e0 = np.array([1.0, 0.0, 0.0])
+    assert d2.push_vector(e0, A3, ex2)
+    assert not d2.push_vector(e0, A3, ex2)
+    assert d2.rank() == 1 and d2.skipped_updates() >= 1
+    assert not d2.push_vector(np.zeros(3), A3, ex2)
+
+
+def test_deflator_apply_dense_formula(torch_cuda):
+    # test_deflation.cpp:103-142 (seed 77 style: random SPD, 4 random candidates)
+    rng = np.random.default_rng(77)
+    n, r = 30, 4
+    gm = rng.standard_normal((n, n))
+    a = gm.T @ gm + n * np.eye(n)
+    A = pg.CsrMatrix(n, np.arange(0, n * n + 1, n, dtype=np.uint32),
+                     np.tile(np.arange(n, dtype=np.uint32), n), a.ravel())
+    ex = pg.DeviceExecutor()
+    d = pg.Deflator()
+    for j in range(r):
+        assert d.push_vector(rng.standard_normal(n), A, ex)
+    d.observe_ritz(123.5)
+    U = d.basis_matrix()
+    t = U.T @ a @ U
+    minv = np.eye(n) + U @ (123.5 * np.linalg.inv(t) - np.eye(r)) @ U.T
+    v = rng.standard_normal(n)
+    assert np.abs(d.apply(v) - minv @ v).max() < 1e-11
+    d.reset()
+    assert d.rank() == 0 and d.mu() == 0.0 and d.history() == []
+    assert np.array_equal(d.apply(v), v)
+
+
+def test_deflator_exact_eigenvectors_to_mu(torch_cuda):
+    # test_deflation.cpp:144-170
+    ex = pg.DeviceExecutor()
+    dvals = np.arange(1, 9, dtype=np.float64)
+    A = _diag(dvals)
+    d = pg.Deflator()
+    for i in (1, 4):
+        e = np.zeros(8)
+        e[i] = 1.0
+        assert d.push_vector(e, A, ex)
+    d.observe_ritz(8.0)
+    for i in (1, 4):
+        e = np.zeros(8)
+        e[i] = 1.0
+        aw = dvals * d.apply(e)
+        want = np.zeros(8)
+        want[i] = 8.0
+        assert np.abs(aw - want).max() < 1e-13
+    e6 = np.zeros(8)
+    e6[6] = 1.0
+    assert np.abs(d.apply(e6) - e6).max() < 1e-13
+
+
+def test_report_csv_round_trip(torch_cuda, ref):
+    A, _, b = _csr(ref, 1)
+    ex = pg.DeviceExecutor()
+    x = np.zeros(A.n)
+    rep = pg.gmres_restarted(A, None, b, x,
+                             pg.GmresConfig(m=4, max_restarts=3, fixed_iterations=True), ex)
+    lines = rep.write_csv().strip().split("\n")
+    assert lines[0] == "restart,inner_step,monitored_residual,explicit_residual"
+    closing = 0
+    for i, line in enumerate(lines[1:]):
+        r, k, mon, tail = line.split(",")
+        assert float(mon) == rep.monitored[i]
+        if tail:
+            assert float(tail) == rep.explicit_residual[int(r)]
+            closing += 1
+    assert closing == len(rep.explicit_residual)

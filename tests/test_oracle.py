@@ -1,0 +1,112 @@
+"""CPU: pin the oracles.  oracle/_ref is the reference compiled verbatim; its
+outputs must reproduce the reference's own logged results
+(proj/test_output.txt:158-168) and the survey probe values, and the numpy
+restatement (oracle/pgmres_oracle.py) must agree with it."""
+import numpy as np
+import pytest
+
+from oracle import pgmres_oracle as O
+
+
+def test_golden_matches_reference_log(golden):
+    # criterion 10 (test_output.txt:168): rank 5, |mu| = 61.27
+    c10 = golden("crit10_diag")
+    assert int(c10["rank"]) == 5
+    assert abs(float(c10["mu"]) - 61.27) < 0.005
+    # criterion 3 mid-flight (test_output.txt:161): restart 3 explicit residual
+    c3 = golden("crit3_ne25")
+    assert float(c3["defl_explicit"][2]) == pytest.approx(3.99e-08, rel=2e-3)
+    assert float(c3["plain_explicit"][2]) == pytest.approx(1.73e-06, rel=3e-3)
+    # criterion 7 (test_output.txt:165): Newton n_e=8 converges in 8 iterations
+    nw = golden("newton_ne8")
+    assert bool(nw["converged"]) and len(nw["inner"]) == 8
+    assert float(nw["u"].max()) == pytest.approx(1.323002464567, abs=1e-11)
+    # survey probe: cfg1 4 restarts / 104 inner, cfg2 9 / 418, beta0 of cfg2
+    c1 = golden("cfg1_defl")
+    assert int(c1["restarts"]) == 4 and int(c1["total_inner"]) == 104 and int(c1["rank"]) == 4
+    c2 = golden("cfg2_defl")
+    assert int(c2["restarts"]) == 9 and int(c2["total_inner"]) == 418
+    assert float(c2["beta0"]) == pytest.approx(0.0079244614604419717, rel=1e-14)
+
+
+def test_reference_build_reproduces_crit10(ref):
+    r = ref.solve(ref.diag_csr(np.arange(1, 51)), np.full(50, 1 / np.sqrt(50)), m=8,
+                  max_restarts=5, fixed_iterations=True)
+    assert r.rank == 5 and abs(r.mu - 61.265) < 1e-3
+
+
+def test_reference_spmv_equals_scipy(ref):
+    A, b = ref.first_newton_system(4)
+    x = np.random.default_rng(11).uniform(-1, 1, A.n)
+    M = O.csr_matrix(A.n, A.row_ptr, A.col_idx, A.values)
+    assert np.array_equal(ref.spmv(A, x), O.spmv(M, x))
+
+
+def _system(golden_name, ref, ne):
+    A, b = ref.first_newton_system(ne)
+    return O.csr_matrix(A.n, A.row_ptr, A.col_idx, A.values), b
+
+
+@pytest.mark.parametrize("orth", ["mgs", "cgs2"])
+def test_numpy_oracle_matches_reference_cfg1(ref, golden, orth):
+    M, b = _system("cfg1_defl", ref, 10)
+    g = golden("cfg1_defl")
+    x = np.zeros(M.shape[0])
+    d = O.Deflator()
+    rep = O.deflated_gmres(M, b, x, O.GmresConfig(m=30, rel_tol=1e-10), d, orth=orth)
+    assert rep.restarts == int(g["restarts"]) and rep.total_inner == int(g["total_inner"])
+    b0 = float(g["beta0"])
+    assert np.max(np.abs(rep.monitored - g["monitored"])) <= 1e-10 * b0
+    assert np.max(np.abs(np.array(rep.explicit_residual) - g["explicit_residual"])) <= 1e-10 * b0
+    assert np.linalg.norm(x - g["x"]) <= 1e-8 * np.linalg.norm(g["x"])
+    assert d.r == int(g["rank"]) and d.mu == pytest.approx(float(g["mu"]), rel=1e-9)
+
+
+def test_numpy_oracle_truncation_run(ref, golden):
+    # run to the rounding floor: rank history and residual floor agree, and the
+    # basis algebra holds (criterion 8, acceptance.cpp:416-427)
+    M, b = _system("ne4_fixed_trunc", ref, 4)
+    g = golden("ne4_fixed_trunc")
+    x = np.zeros(M.shape[0])
+    d = O.Deflator()
+    rep = O.deflated_gmres(M, b, x, O.GmresConfig(m=10, max_restarts=26, fixed_iterations=True), d)
+    assert [h[1] for h in d.history] == list(g["hist_r"])
+    b0 = float(g["beta0"])
+    assert np.max(np.abs(np.array(rep.explicit_residual) - g["explicit_residual"])) <= 1e-10 * b0
+    U = d.U[:, : d.r]
+    assert np.abs(U.T @ U - np.eye(d.r)).max() < 1e-10
+    T = d.T_block()
+    assert np.abs(T - U.T @ (M @ U)).max() < 1e-10 * np.abs(T).max()
+
+
+def test_numpy_oracle_truncation_matches_reference(ref, golden):
+    # four truncations while the residual is still 1e-3: T and mu comparable
+    M, b = _system("ne10_m4_trunc", ref, 10)
+    g = golden("ne10_m4_trunc")
+    x = np.zeros(M.shape[0])
+    d = O.Deflator()
+    O.deflated_gmres(M, b, x, O.GmresConfig(m=4, max_restarts=24, fixed_iterations=True), d)
+    assert [h[1] for h in d.history] == list(g["hist_r"])
+    assert np.abs(d.T_block() - g["T"]).max() <= 1e-8 * np.abs(g["T"]).max()
+    assert d.mu == pytest.approx(float(g["mu"]), rel=1e-9)
+    assert np.linalg.norm(x - g["x"]) <= 1e-10 * np.linalg.norm(g["x"])
+
+
+def test_numpy_oracle_dense_lu(golden):
+    s = golden("ne2_system")
+    n = s["rhs"].size
+    M = O.csr_matrix(n, s["row_ptr"], s["col_idx"], s["values"])
+    x = np.zeros(n)
+    O.deflated_gmres(M, s["rhs"], x, O.GmresConfig(m=50, rel_tol=1e-12), O.Deflator())
+    xd = np.linalg.solve(M.toarray(), s["rhs"])
+    assert np.linalg.norm(x - xd) <= 1e-10 * np.linalg.norm(xd)
+
+
+def test_numpy_oracle_errors():
+    with pytest.raises(ValueError):
+        O.Workspace(4, 0)
+    with pytest.raises(ValueError):
+        O.Deflator(O.DeflationConfig(r_max=0))
+    bad = lambda v: np.full_like(v, np.nan)  # noqa: E731
+    with pytest.raises(O.GmresError):
+        O.gmres_restarted(bad, None, np.ones(2), np.zeros(2), O.GmresConfig())
