@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""Benchmark of the deflated PGMRES hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl pgmres|reference]
+
+One step = one complete deflated_gmres solve of the first Newton system
+J(0) x = -R(0) of the 3-D Bratu FEM problem (lambda = 6.8, x0 = 0),
+GMRES(50) + deflation (r_max = 20), rel_tol = 1e-10.  Default workload is
+BASELINE config 2: n_e = 50, 1,030,301 DOF, 62,606,425 nnz (the matrix,
+751 MB, is larger than the 126 MB L2, so no L2 flush is needed).
+
+`value`  : GMRES iterations/s with inputs resident in HBM (CUDA events on the
+           library stream, max over ranks).
+`e2e`    : same metric through the public API with HOST buffers: full CSR
+           upload + b + x0 host->device, solve, x device->host, every step.
+`roofline`: the step SpMV kernel (SpMV fused with the deflation correction and
+           the CGS2 pass-1 dots), algorithmic bytes / its CUDA-event duration.
+`cpu_baseline`: the reference CPU solver (oracle/_ref, the reference's own
+           sources) on a bounded sample of the same system, all host cores.
+--impl reference: the reference CPU solver itself, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LAMBDA = 6.8
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="pgmres", choices=["pgmres", "reference"])
+    ap.add_argument("--ne", type=int, default=50)
+    ap.add_argument("--m", type=int, default=50)
+    ap.add_argument("--tol", type=float, default=1e-10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def metric_name(a):
+    return (f"PGMRES fp64 GMRES iterations/s (deflated GMRES({a.m}), rel_tol {a.tol:g}, "
+            f"time-to-solution per step)")
+
+
+def workload(a, n, nnz):
+    return {"workload": f"cfg2-equivalent: 3-D Bratu first Newton system, n_e={a.ne} "
+                        f"({n:,} DOF, {nnz:,} nnz), GMRES({a.m}) + deflation r_max=20, "
+                        f"rel_tol={a.tol:g}, x0=0",
+            "n_e": a.ne, "dof": n, "nnz": nnz, "m": a.m, "rel_tol": a.tol, "r_max": 20,
+            "lambda": LAMBDA,
+            "l2": "inputs larger than L2 (matrix 12*nnz bytes >> 126 MB); no flush",
+            "parallelism": f"z-slab row blocks x{a.gpus}" if a.gpus > 1 else "1 GPU"}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return PEAKS_FALLBACK["hbm_gbs"], "fallback"
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.lines = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.th:
+            self.th.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def step_spmv_bytes(n, nnz, k, r):
+    """Algorithmic HBM bytes of one fused step-SpMV launch:
+    SpMV 12 nnz + 4(n+1) + 8n (x) + 8n (w), + 8n(k+1) basis reads for the
+    CGS2 pass-1 dots, + 8n r AU reads for the deflation correction."""
+    return 12 * nnz + 4 * (n + 1) + 16 * n + 8 * n * (k + 1) + 8 * n * r
+
+
+def class_bytes(cls, n, nnz, k, r, steps):
+    spmv = 12 * nnz + 4 * (n + 1) + 16 * n
+    if cls == 0:
+        return step_spmv_bytes(n, nnz, k, r)
+    if cls == 1:  # w1 = w - V h1 (read V_0..k, w; write w) ; dots from smem
+        return 8 * n * (k + 3)
+    if cls == 2:  # w2 = w1 - V h2, ||w2||, U^T w2
+        return 8 * n * (k + 3 + r)
+    if cls == 3:  # x += V y + U c
+        return 8 * n * (steps + r + 2)
+    if cls == 8:  # r = b - A x, ||r||, U^T r
+        return spmv + 8 * n + 8 * n * r
+    return 0
+
+
+def run_gpu(a):
+    import torch
+
+    import paper_1906_04051_b200 as pg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    nccl_id = None
+    na = 2 * a.ne + 1
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_1906_04051_b200.dgmres import nccl_unique_id
+
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy())
+    ex = pg.DeviceExecutor(local, n_global=na ** 3, n_axis=na if world > 1 else 0, rank=rank,
+                           world=world, nccl_id=nccl_id)
+    A_d, b_d = ex.assemble_bratu(a.ne, LAMBDA, device=True)
+    n = ex.n_own
+    nnz_local = A_d.nnz
+    dA = ex.upload(A_d)
+    ext = torch.cuda.ExternalStream(ex.stream())
+    x_d = torch.zeros(n, dtype=torch.float64, device="cuda")
+    d = pg.Deflator(pg.DeflationConfig(r_max=20), ex)
+    cfg = pg.GmresConfig(m=a.m, max_restarts=100, rel_tol=a.tol)
+
+    def step():
+        d.reset()
+        with torch.cuda.stream(ext):
+            x_d.zero_()
+        return pg.deflated_gmres(dA, b_d, x_d, cfg, d, ex)
+
+    for _ in range(a.warmup):
+        rep = step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    iters = 0
+    launches = 0
+    reps = []
+    torch.cuda.synchronize()
+    ev0.record(ext)
+    for _ in range(a.steps):
+        rep = step()
+        iters += rep.total_inner
+        launches += ex.launch_count()
+        reps.append(rep)
+    ev1.record(ext)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    t = ev0.elapsed_time(ev1) / 1e3
+    if dist:
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    value = iters / t
+    ms_per_step = 1e3 * t / a.steps
+    last = reps[-1]
+
+    # ---- roofline: per-launch CUDA-event profile of one more solve -------------
+    ex.set_profiling(True)
+    prep = step()
+    ex.set_profiling(False)
+    cls, cyc, kk, ms = ex.profile()
+    hist = d.history()
+    rank_of = {0: 0}
+    for h in hist:
+        rank_of[h.restart + 1] = h.r
+    steps_of = {}
+    for r_, k_ in zip(prep.inner_restart, prep.inner_step):
+        steps_of[int(r_)] = max(steps_of.get(int(r_), 0), int(k_) + 1)
+    n_g = na ** 3 if world > 1 else n
+    per = {}
+    for c, y, k, t_ms in zip(cls, cyc, kk, ms):
+        c, y, k = int(c), int(y), int(k)
+        if c in (0, 1, 2) and (y not in steps_of or k >= steps_of[y]):
+            continue  # early-exit launch after the cycle stopped
+        rr = rank_of.get(y, 0)
+        b = class_bytes(c, n, nnz_local, k, rr, steps_of.get(y, a.m))
+        e = per.setdefault(c, [0.0, 0.0, 0])
+        e[0] += b
+        e[1] += t_ms / 1e3
+        e[2] += 1
+    names = {0: "step_spmv", 1: "cgs2_pass2_dots", 2: "cgs2_update_norm", 3: "x_update",
+             4: "ritz", 5: "push_sweeps", 6: "push_spmv", 7: "rotate", 8: "residual_spmv",
+             9: "other"}
+    prof_total = float(ms.sum()) / 1e3
+    kernels = {names[c]: {"launches": v[2], "ms_total": round(1e3 * v[1], 3),
+                          "share": round(v[1] / prof_total, 4) if prof_total else None,
+                          "GBps": round(v[0] / v[1] / 1e9, 1) if v[0] and v[1] else None}
+               for c, v in sorted(per.items())}
+    peak, peak_kind = peaks()
+    sp = per.get(0, [0, 1, 1])
+    achieved = sp[0] / sp[1] / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "kernel": "k_spmv<StepEpi> (SpMV + AU c deflation + CGS2 pass-1 dots)",
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "bytes_per_launch_avg": int(sp[0] / max(1, sp[2])),
+                "launch_ms_avg": round(1e3 * sp[1] / max(1, sp[2]), 4)}
+    tot_bytes = sum(v[0] for v in per.values())
+    tot_time = sum(v[1] for v in per.values())
+    solve_frac = (tot_bytes / prof_total / 1e9) / peak if prof_total else None
+
+    # ---- e2e through the public API with host buffers --------------------------
+    e2e = None
+    if not a.no_e2e:
+        rp_h = torch.empty(n + 1, dtype=torch.int32, pin_memory=True)
+        ci_h = torch.empty(nnz_local, dtype=torch.int32, pin_memory=True)
+        va_h = torch.empty(nnz_local, dtype=torch.float64, pin_memory=True)
+        b_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        x_h = torch.zeros(n, dtype=torch.float64, pin_memory=True)
+        rp_h.copy_(A_d.row_ptr)
+        ci_h.copy_(A_d.col_idx)
+        va_h.copy_(A_d.values)
+        b_h.copy_(b_d)
+        A_h = pg.CsrMatrix(n, rp_h.numpy().view(np.uint32), ci_h.numpy().view(np.uint32),
+                           va_h.numpy())
+        bn, xn = b_h.numpy(), x_h.numpy()
+
+        def e2e_step():
+            d.reset()
+            xn[:] = 0.0
+            return pg.deflated_gmres(A_h, bn, xn, cfg, d, ex)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e_iters = 0
+        e0.record(ext)
+        for _ in range(a.steps):
+            e_iters += e2e_step().total_inner
+        e1.record(ext)
+        torch.cuda.synchronize()
+        te = e0.elapsed_time(e1) / 1e3
+        if dist:
+            tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": round(e_iters / te, 2), "unit": "iter/s",
+               "h2d_bytes_per_step": int(4 * (n + 1) + 12 * nnz_local + 16 * n),
+               "d2h_bytes_per_step": int(8 * n),
+               "ms_per_step": round(1e3 * te / a.steps, 3),
+               "path": "deflated_gmres(CsrMatrix host arrays, numpy b, x) -> pgm_matrix_upload"
+                       " + pgm_solve(host pointers)"}
+
+    out = {
+        "metric": metric_name(a), "value": round(value, 2), "unit": "iter/s",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: Bratu FEM Jacobian/residual assembled on the GPU by "
+                "pgm_bratu_assemble (bit-identical to the reference assembly at u=0)",
+        "config": workload(a, n_g, A_d.nnz if world == 1 else None),
+        "gpu_launches": int(launches),
+        "iterations_per_step": int(last.total_inner), "restarts_per_step": int(last.restarts),
+        "final_relative": last.final_relative,
+        "time_to_solution_s": round(ms_per_step / 1e3, 5),
+        "roofline": roofline,
+        "solve_roofline": {"frac": round(solve_frac, 4) if solve_frac else None,
+                           "achieved_GBps": round(tot_bytes / prof_total / 1e9, 1)
+                           if prof_total else None,
+                           "note": "all hot-path kernels of one profiled solve, algorithmic "
+                                   "bytes / summed kernel time"},
+        "spmv_GBps": round(achieved, 1),
+        "kernels": kernels,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(a)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+def _ref_threads(na):
+    return max(1, min(os.cpu_count() or 1, na))
+
+
+def cpu_baseline(a):
+    """The reference CPU solver (oracle/_ref: its own sources) on a bounded
+    sample of the same system: 2 fixed restart cycles (2m inner iterations)."""
+    from oracle import refbind as R
+
+    na = 2 * a.ne + 1
+    th = _ref_threads(na)
+    A, b = R.first_newton_system(a.ne, LAMBDA, threads=th)
+    r = R.solve(A, b, m=a.m, max_restarts=2, fixed_iterations=True, ne=a.ne, threads=th)
+    return {"value": round(r.total_inner / r.wall_s, 3), "unit": "iter/s", "cores": th,
+            "kind": "reference",
+            "sample": f"2 fixed restart cycles ({r.total_inner} inner iterations) of deflated "
+                      f"GMRES({a.m}) on the same n_e={a.ne} system, deterministic executor, "
+                      f"{th} threads, {r.wall_s:.2f} s",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import refbind as R
+
+    na = 2 * a.ne + 1
+    th = _ref_threads(na)
+    A, b = R.first_newton_system(a.ne, LAMBDA, threads=th)
+    kw = dict(m=a.m, ne=a.ne, threads=th)
+    full = R.solve(A, b, max_restarts=100, rel_tol=a.tol, **kw)  # warm-up 0: full solve
+    if full.wall_s <= 20.0:
+        sample = dict(max_restarts=100, rel_tol=a.tol)
+        desc = f"full tolerance solve ({full.total_inner} inner iterations)"
+    else:
+        sample = dict(max_restarts=1, fixed_iterations=True)
+        desc = f"1 fixed restart cycle ({a.m} inner iterations)"
+    for _ in range(max(0, a.warmup - 1)):
+        R.solve(A, b, **sample, **kw)
+    iters, secs = 0, 0.0
+    for _ in range(a.steps):
+        r = R.solve(A, b, **sample, **kw)
+        iters += r.total_inner
+        secs += r.wall_s
+    v = iters / secs
+    out = {"metric": metric_name(a), "value": round(v, 3), "unit": "iter/s", "n_gpus": a.gpus,
+           "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 * secs / a.steps, 3),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic: Bratu FEM first Newton system (reference assembly)",
+           "config": workload(a, A.n, A.nnz), "impl": "reference",
+           "cpu_baseline": {"value": round(v, 3), "unit": "iter/s", "cores": th,
+                            "kind": "reference",
+                            "sample": f"{desc} per step, reference deflated_gmres "
+                                      f"(oracle/_ref), deterministic executor, {th} threads",
+                            "cpu_model": _cpu_model()},
+           "e2e": {"value": round(v, 3), "unit": "iter/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_gpu(a)
+
+
+if __name__ == "__main__":
+    main()

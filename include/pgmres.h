@@ -158,8 +158,29 @@ pgm_status pgm_solve(pgm_context* ctx, pgm_matrix* a, pgm_deflator* d, const dou
                      double* x, const pgm_gmres_config* cfg, int32_t flags, pgm_report* rep);
 void pgm_report_free(pgm_report* rep);
 
+/* 128-byte ncclUniqueId for pgm_context_config.nccl_id (call on rank 0 and
+ * broadcast it, e.g. with torch.distributed). */
+pgm_status pgm_nccl_unique_id(void* out128);
+
 /* Kernel launches of the last pgm_solve (evidence for the bench). */
 uint64_t pgm_context_launch_count(const pgm_context* ctx);
+/* Optional CUDA-event timing of every hot-path kernel of the next solves
+ * (class ids: 0 step SpMV, 1 CGS2 pass-2 dots, 2 CGS2 update+norm, 3 x update,
+ * 4 Ritz, 5 push sweeps, 6 push SpMV, 7 rotate, 8 residual, 9 other). */
+pgm_status pgm_context_set_profiling(pgm_context* ctx, int32_t on);
+uint32_t pgm_context_profile(pgm_context* ctx, uint32_t* cls, uint32_t* cycle, uint32_t* k,
+                             float* ms, uint32_t cap);
+
+/* ---- caller side: FEM assembly of the Bratu system ---------------------- *
+ * pattern_nnz / symbolic_pattern / assemble_jacobian / assemble_residual
+ * (assembly.hpp:32-49) on the device for the context's owned rows: writes
+ * row_ptr (n_own + 1), col_idx, values (nnz) and rhs = -R(u) (n_own).  u is the
+ * global iterate (NULL = 0, the first Newton system).  Bit-identical to the
+ * reference assembly at u = 0. */
+pgm_status pgm_bratu_nnz(const pgm_context* ctx, uint32_t n_e, uint64_t* nnz);
+pgm_status pgm_bratu_assemble(pgm_context* ctx, uint32_t n_e, double lambda, const double* u,
+                              int32_t flags, uint32_t* row_ptr, uint32_t* col_idx,
+                              double* values, double* rhs);
 
 #ifdef __cplusplus
 }

@@ -60,7 +60,8 @@ EXPORTS = [
     "pgm_deflator_destroy", "pgm_deflator_reset", "pgm_deflator_info", "pgm_deflator_history",
     "pgm_deflator_basis", "pgm_deflator_push", "pgm_deflator_truncate",
     "pgm_deflator_observe_ritz", "pgm_deflator_apply", "pgm_solve", "pgm_report_free",
-    "pgm_context_launch_count",
+    "pgm_context_launch_count", "pgm_context_set_profiling", "pgm_context_profile",
+    "pgm_bratu_nnz", "pgm_bratu_assemble", "pgm_nccl_unique_id",
 ]
 
 _lib = None
@@ -104,6 +105,11 @@ def lib():
         "pgm_solve": ([vp, vp, vp, vp, vp, C.POINTER(GmresConfigC), i32, C.POINTER(ReportC)],
                       C.c_int),
         "pgm_report_free": ([C.POINTER(ReportC)], None),
+        "pgm_context_set_profiling": ([vp, i32], C.c_int),
+        "pgm_context_profile": ([vp, vp, vp, vp, vp, u32], u32),
+        "pgm_bratu_nnz": ([vp, u32, C.POINTER(C.c_uint64)], C.c_int),
+        "pgm_bratu_assemble": ([vp, u32, dbl, vp, i32, vp, vp, vp, vp], C.c_int),
+        "pgm_nccl_unique_id": ([vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -16,6 +16,9 @@
 #include <vector>
 
 #include "../../include/pgmres.h"
+#include <cub/cub.cuh>
+
+#include "bratu.cuh"
 #include "kernels.cuh"
 #include "nccl_lite.h"
 
@@ -99,6 +102,16 @@ struct pgm_context {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // multi-GPU
   void* nccl = nullptr;
+  // optional per-launch profiling (CUDA events around every hot-path kernel)
+  bool prof_on = false;
+  int prof_cycle = 0;
+  struct Rec {
+    uint32_t cls, cyc, k;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
 };
 
 struct pgm_matrix {
@@ -162,6 +175,64 @@ int occupancy(K kernel, int threads, size_t smem) {
 
 constexpr int MAX_BLOCKS_PER_SM = 4;  // bounds the grid-reduction tail
 
+// Kernel classes of the profile (pgm_context_profile).
+enum ProfClass : uint32_t {
+  PC_STEP_SPMV = 0, PC_SWEEP_B = 1, PC_SWEEP_C = 2, PC_XUPDATE = 3, PC_RITZ = 4,
+  PC_PUSH = 5, PC_PUSH_SPMV = 6, PC_ROTATE = 7, PC_RESIDUAL = 8, PC_OTHER = 9
+};
+
+cudaEvent_t prof_event(pgm_context* ctx) {
+  if (ctx->ev_used == ctx->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->ev_pool.push_back(e);
+  }
+  return ctx->ev_pool[ctx->ev_used++];
+}
+
+struct ProfScope {
+  pgm_context* ctx;
+  pgm_context::Rec rec{};
+  ProfScope(pgm_context* c, uint32_t cls, uint32_t k) : ctx(c) {
+    if (!ctx->prof_on) return;
+    rec.cls = cls;
+    rec.cyc = (uint32_t)ctx->prof_cycle;
+    rec.k = k;
+    rec.a = prof_event(ctx);
+    rec.b = prof_event(ctx);
+    cudaEventRecord(rec.a, ctx->stream);
+  }
+  ~ProfScope() {
+    if (!ctx->prof_on) return;
+    cudaEventRecord(rec.b, ctx->stream);
+    ctx->prof.push_back(rec);
+  }
+};
+
+template <class Epi>
+uint32_t prof_class_of() {
+  return PC_OTHER;
+}
+template <>
+uint32_t prof_class_of<StepEpi>() {
+  return PC_STEP_SPMV;
+}
+template <>
+uint32_t prof_class_of<ResidualEpi>() {
+  return PC_RESIDUAL;
+}
+template <>
+uint32_t prof_class_of<PushEpi>() {
+  return PC_PUSH_SPMV;
+}
+template <int MODE>
+uint32_t prof_class_sweep() {
+  return MODE == SW_CGS2_B ? PC_SWEEP_B
+       : MODE == SW_CGS2_C ? PC_SWEEP_C
+       : MODE == SW_XUPDATE ? PC_XUPDATE
+       : (MODE >= SW_PUSH1 && MODE <= SW_PUSH3) ? PC_PUSH : PC_OTHER;
+}
+
 size_t spmv_smem(int nv) { return sizeof(double) * (EPI_SMALL + 2 * TILE + 33 * (size_t)nv); }
 size_t sweep_smem(int np, int np2, int nv, bool staged) {
   return sizeof(double) *
@@ -170,10 +241,11 @@ size_t sweep_smem(int np, int np2, int nv, bool staged) {
 
 template <class Epi>
 Status launch_spmv(pgm_context* ctx, const pgm_matrix* A, const Params& P, const Epi& E,
-                   int nvmax) {
+                   int nvmax, uint32_t prof_k = 0) {
   const size_t smem = spmv_smem(nvmax);
   const int occ = std::min(MAX_BLOCKS_PER_SM, occupancy(k_spmv<Epi>, SPMV_THREADS, smem));
   const int G = std::max(1, std::min(A->ntiles, occ * ctx->nsm));
+  ProfScope ps(ctx, prof_class_of<Epi>(), prof_k);
   k_spmv<Epi><<<G, SPMV_THREADS, smem, ctx->stream>>>(A->view(), P, E);
   ctx->launches++;
   CU(cudaGetLastError());
@@ -187,6 +259,7 @@ Status launch_sweep(pgm_context* ctx, const Params& P, int k, int np, int np2, i
   const int occ = std::min(MAX_BLOCKS_PER_SM, occupancy(k_sweep<MODE>, SW_THREADS, smem));
   const int nchunks = (int)((ctx->n + CH - 1) / CH);
   const int G = std::max(1, std::min(nchunks, occ * ctx->nsm));
+  ProfScope ps(ctx, prof_class_sweep<MODE>(), (uint32_t)k);
   k_sweep<MODE><<<G, SW_THREADS, smem, ctx->stream>>>(P, k);
   ctx->launches++;
   CU(cudaGetLastError());
@@ -407,7 +480,7 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
   for (int k = 0; k < m; ++k) {
     if (ctx->world > 1) TRY(halo_exchange(ctx, ctx->V + (size_t)k * ctx->ld));
     StepEpi se{k};
-    TRY(launch_spmv(ctx, A, P, se, m + 1));
+    TRY(launch_spmv(ctx, A, P, se, m + 1, (uint32_t)k));
     TRY(finish_global<100>(ctx, P, k, k + 1));
     TRY(launch_sweep<SW_CGS2_B>(ctx, P, k, m + 1, 0, m + 1, true));
     TRY(finish_global<SW_CGS2_B>(ctx, P, k, k + 1));
@@ -419,7 +492,10 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
     const size_t rsmem = sizeof(double) * (2 * (size_t)m * m + 4 * m);
     if (rsmem > 48 * 1024)
       CU(cudaFuncSetAttribute(k_ritz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
-    k_ritz<<<1, RITZ_THREADS, rsmem, ctx->stream>>>(P);
+    {
+      ProfScope ps(ctx, PC_RITZ, 0);
+      k_ritz<<<1, RITZ_THREADS, rsmem, ctx->stream>>>(P);
+    }
     ctx->launches++;
     CU(cudaGetLastError());
     TRY(launch_sweep<SW_PUSH1>(ctx, P, 1, m, 0, R1 + 1, false));
@@ -431,7 +507,10 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
     if (ctx->world > 1) TRY(halo_exchange(ctx, d->u));
     TRY(launch_spmv(ctx, A, P, PushEpi{}, 2 * R1 + 1));
     TRY(finish_global<102>(ctx, P, 0, -1));
-    k_rotate<true><<<ctx->nsm * 4, 256, 0, ctx->stream>>>(P);
+    {
+      ProfScope ps(ctx, PC_ROTATE, 0);
+      k_rotate<true><<<ctx->nsm * 4, 256, 0, ctx->stream>>>(P);
+    }
     ctx->launches++;
     CU(cudaGetLastError());
   }
@@ -516,12 +595,16 @@ Status solve_impl(pgm_context* ctx, pgm_matrix* A, pgm_deflator* dflt, const dou
   CU(cudaMemcpyAsync(ctx->g, &gs, sizeof(GState), cudaMemcpyHostToDevice, ctx->stream));
   const Params P = make_params(ctx, d);
   ctx->launches = 0;
+  ctx->prof.clear();
+  ctx->ev_used = 0;
+  ctx->prof_cycle = -1;
   CU(cudaEventRecord(ctx->ev0, ctx->stream));
   if (ctx->world > 1) TRY(halo_exchange(ctx, ctx->x));
   TRY(launch_spmv(ctx, A, P, ResidualEpi{1}, d->R1 + 1));
   TRY(finish_global<101>(ctx, P, 1, -1));
   TRY(read_status(ctx));
   while (!ctx->h_status->done) {
+    ctx->prof_cycle = ctx->h_status->restart;
     TRY(enqueue_cycle(ctx, A, d, P, harvest));
     TRY(read_status(ctx));
   }
@@ -1174,6 +1257,178 @@ void pgm_report_free(pgm_report* rep) {
   std::free(rep->explicit_residual);
   rep->inner_restart = rep->inner_step = nullptr;
   rep->inner_monitored = rep->explicit_residual = nullptr;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Profiling + device FEM assembly entry points
+namespace {
+
+uint64_t bratu_rows_nnz(uint32_t n_e, uint32_t row_begin, uint32_t row_end) {
+  const uint32_t na = 2 * n_e + 1, last = na - 1;
+  uint64_t total = 0;
+  uint32_t lo;
+  for (uint64_t v = row_begin; v < row_end; ++v) {
+    const uint32_t ix = (uint32_t)(v % na), iy = (uint32_t)((v / na) % na),
+                   iz = (uint32_t)(v / ((uint64_t)na * na));
+    if (ix == 0 || ix == last || iy == 0 || iy == last)
+      total += 1;
+    else
+      total += (uint64_t)bratu::reach(ix, last, &lo) * bratu::reach(iy, last, &lo) *
+               bratu::reach(iz, last, &lo);
+  }
+  return total;
+}
+
+Status bratu_assemble(pgm_context* ctx, uint32_t n_e, double lambda, const double* u,
+                      int32_t flags, uint32_t* row_ptr, uint32_t* col_idx, double* values,
+                      double* rhs) {
+  const uint64_t na = 2ull * n_e + 1;
+  if (n_e == 0) return einval("build_mesh: n_e must be positive");
+  if (na * na * na != ctx->n_global)
+    return einval("bratu: (2 n_e + 1)^3 != context n_global");
+  static bool table_done = false;
+  if (!table_done) {
+    bratu::Table t;
+    bratu::build_table(t);
+    CU(cudaMemcpyToSymbol(bratu::c_tab, &t, sizeof(t)));
+    table_done = true;
+  }
+  const uint32_t rb = ctx->part.row_begin, re = ctx->part.row_end;
+  const uint64_t nnz = bratu_rows_nnz(n_e, rb, re);
+  if (nnz > 0xFFFFFFFFull) return Status{PGM_EINVAL, "symbolic_pattern: nnz exceeds 32-bit offsets"};
+  const bool dev = (flags & PGM_DEVICE_PTRS) != 0;
+  const uint32_t nrows = re - rb;
+  cudaStream_t st = ctx->stream;
+  unsigned* d_rp = nullptr;
+  unsigned* d_ci = nullptr;
+  double *d_va = nullptr, *d_rhs = nullptr, *d_u = nullptr, *d_f = nullptr;
+  void* d_tmp = nullptr;
+  struct Guard {
+    std::vector<void*> p;
+    ~Guard() {
+      for (void* q : p) cudaFree(q);
+    }
+  } guard;
+  auto own = [&](auto** ptr, size_t count) -> Status {
+    TRY(dalloc(ptr, count));
+    guard.p.push_back((void*)*ptr);
+    return {};
+  };
+  if (dev) {
+    d_rp = row_ptr;
+    d_ci = col_idx;
+    d_va = values;
+    d_rhs = rhs;
+  } else {
+    TRY(own(&d_rp, (size_t)nrows + 1));
+    TRY(own(&d_ci, nnz));
+    TRY(own(&d_va, nnz));
+    TRY(own(&d_rhs, nrows));
+  }
+  if (u) {
+    if (dev) {
+      d_u = const_cast<double*>(u);
+    } else {
+      TRY(own(&d_u, ctx->n_global));
+      CU(cudaMemcpyAsync(d_u, u, 8 * (size_t)ctx->n_global, cudaMemcpyHostToDevice, st));
+    }
+  }
+  bratu::Mesh M;
+  M.n_e = n_e;
+  M.na = (uint32_t)na;
+  M.plane = na * na;
+  M.row_begin = rb;
+  M.nrows = nrows;
+  M.lambda = lambda;
+  const double h_e = 1.0 / n_e;
+  M.vol = std::pow(h_e / 2.0, 3);
+  M.stiff_sc = h_e / 2.0;
+  const unsigned T = 256;
+  bratu::k_row_len<<<(unsigned)((nrows + T - 1) / T), T, 0, st>>>(M, d_rp);
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, d_rp + 1, d_rp + 1, (int)nrows, st);
+  TRY(own((char**)&d_tmp, tmp_bytes));
+  cub::DeviceScan::InclusiveSum(d_tmp, tmp_bytes, d_rp + 1, d_rp + 1, (int)nrows, st);
+  bratu::k_cols<<<(unsigned)((nrows + T - 1) / T), T, 0, st>>>(M, d_rp, d_ci, d_va);
+  const uint32_t zb = (uint32_t)(rb / M.plane), ze = (uint32_t)((re + M.plane - 1) / M.plane);
+  const int lay_lo = std::max(0, (int)(zb >> 1) - 1);
+  const int lay_hi = std::min((int)n_e - 1, (int)((ze - 1) >> 1));
+  const uint64_t per_layer = (uint64_t)n_e * n_e;
+  const uint64_t e0 = (uint64_t)lay_lo * per_layer;
+  const uint64_t ecount = (uint64_t)(lay_hi - lay_lo + 1) * per_layer;
+  TRY(own(&d_f, ecount * 27));
+  bratu::k_elem_f<<<(unsigned)((ecount * 27 + T - 1) / T), T, 0, st>>>(M, d_u, d_f, e0, ecount);
+  bratu::k_jac_values<<<(unsigned)(((uint64_t)nrows * 32 + T - 1) / T), T, 0, st>>>(M, d_rp, d_f,
+                                                                                   e0, d_va);
+  bratu::k_residual_rhs<<<(unsigned)((nrows + T - 1) / T), T, 0, st>>>(M, d_u, d_f, e0, d_rhs);
+  CU(cudaGetLastError());
+  if (!dev) {
+    CU(cudaMemcpyAsync(row_ptr, d_rp, 4 * ((size_t)nrows + 1), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(col_idx, d_ci, 4 * nnz, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(values, d_va, 8 * nnz, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(rhs, d_rhs, 8 * (size_t)nrows, cudaMemcpyDeviceToHost, st));
+  }
+  CU(cudaStreamSynchronize(st));
+  return {};
+}
+
+}  // namespace
+
+extern "C" {
+
+pgm_status pgm_nccl_unique_id(void* out128) {
+  if (!out128) return PGM_EINVAL;
+  if (!nccl_lite::available() || nccl_lite::get_unique_id(out128) != 0) {
+    g_tls_err = "ncclGetUniqueId unavailable";
+    return PGM_ENCCL;
+  }
+  return PGM_OK;
+}
+
+pgm_status pgm_context_set_profiling(pgm_context* ctx, int32_t on) {
+  if (!ctx) return PGM_EINVAL;
+  ctx->prof_on = on != 0;
+  return PGM_OK;
+}
+
+uint32_t pgm_context_profile(pgm_context* ctx, uint32_t* cls, uint32_t* cycle, uint32_t* k,
+                             float* ms, uint32_t cap) {
+  if (!ctx) return 0;
+  cudaStreamSynchronize(ctx->stream);
+  const uint32_t n = (uint32_t)std::min<size_t>(cap, ctx->prof.size());
+  for (uint32_t i = 0; i < n; ++i) {
+    const auto& r = ctx->prof[i];
+    if (cls) cls[i] = r.cls;
+    if (cycle) cycle[i] = r.cyc;
+    if (k) k[i] = r.k;
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    if (ms) ms[i] = t;
+  }
+  return n;
+}
+
+pgm_status pgm_bratu_nnz(const pgm_context* ctx, uint32_t n_e, uint64_t* nnz) {
+  if (!nnz || n_e == 0) return PGM_EINVAL;
+  const uint64_t na = 2ull * n_e + 1;
+  uint32_t rb = 0, re = (uint32_t)(na * na * na);
+  if (ctx) {
+    rb = ctx->part.row_begin;
+    re = ctx->part.row_end;
+  }
+  *nnz = bratu_rows_nnz(n_e, rb, re);
+  return PGM_OK;
+}
+
+pgm_status pgm_bratu_assemble(pgm_context* ctx, uint32_t n_e, double lambda, const double* u,
+                              int32_t flags, uint32_t* row_ptr, uint32_t* col_idx, double* values,
+                              double* rhs) {
+  if (!ctx || !row_ptr || !col_idx || !values || !rhs) return PGM_EINVAL;
+  cudaSetDevice(ctx->device);
+  Status s = bratu_assemble(ctx, n_e, lambda, u, flags, row_ptr, col_idx, values, rhs);
+  return s.code ? fail(ctx, s) : PGM_OK;
 }
 
 }  // extern "C"

@@ -233,6 +233,62 @@ class DeviceExecutor:
     def upload(self, A: CsrMatrix) -> "DeviceCsr":
         return DeviceCsr(self, A)
 
+    # ---- caller side: device FEM assembly (assembly.hpp:32-49) ----
+    def bratu_nnz(self, n_e: int) -> int:
+        nnz = C.c_uint64()
+        _check(capi.lib().pgm_bratu_nnz(self._ctx, int(n_e), C.byref(nnz)))
+        return int(nnz.value)
+
+    def assemble_bratu(self, n_e: int, lam: float = 6.8, u=None, device: bool = True):
+        """Newton system J(u) x = -R(u) for this rank's rows, assembled on the GPU.
+
+        Returns (CsrMatrix, rhs); torch CUDA tensors when device=True, numpy
+        arrays otherwise.  u = None is the first Newton system (u = 0)."""
+        na = 2 * int(n_e) + 1
+        self._ensure(na ** 3)
+        nnz = self.bratu_nnz(n_e)
+        n = self.n_own
+        if device:
+            import torch
+
+            rp = torch.empty(n + 1, dtype=torch.int32, device=f"cuda:{self.device}")
+            ci = torch.empty(nnz, dtype=torch.int32, device=rp.device)
+            va = torch.empty(nnz, dtype=torch.float64, device=rp.device)
+            rhs = torch.empty(n, dtype=torch.float64, device=rp.device)
+            ptrs = [t.data_ptr() for t in (rp, ci, va, rhs)]
+            flags = capi.PGM_DEVICE_PTRS
+        else:
+            rp = np.empty(n + 1, np.uint32)
+            ci = np.empty(nnz, np.uint32)
+            va = np.empty(nnz, np.float64)
+            rhs = np.empty(n, np.float64)
+            ptrs = [a.ctypes.data for a in (rp, ci, va, rhs)]
+            flags = 0
+        up = None
+        if u is not None:
+            up, uf, _ku = _ptr(u, np.float64)
+            if uf != flags:
+                raise ValueError("u must live where the outputs are requested")
+        _check(capi.lib().pgm_bratu_assemble(self.handle, int(n_e), float(lam), up, flags, *ptrs),
+               self.handle)
+        return CsrMatrix(n, rp, ci, va), rhs
+
+    # ---- per-kernel CUDA-event profile of the solves run while enabled ----
+    def set_profiling(self, on: bool):
+        _check(capi.lib().pgm_context_set_profiling(self.handle, int(bool(on))), self.handle)
+
+    def profile(self):
+        """(class, cycle, k, ms) arrays of every profiled launch of the last solve."""
+        L = capi.lib()
+        cap = 1 << 20
+        cls = np.zeros(cap, np.uint32)
+        cyc = np.zeros(cap, np.uint32)
+        kk = np.zeros(cap, np.uint32)
+        ms = np.zeros(cap, np.float32)
+        n = L.pgm_context_profile(self.handle, cls.ctypes.data, cyc.ctypes.data, kk.ctypes.data,
+                                  ms.ctypes.data, cap)
+        return cls[:n].copy(), cyc[:n].copy(), kk[:n].copy(), ms[:n].astype(np.float64)
+
     def spmv(self, A, x, y=None):
         """Executor::spmv (parallel.hpp:93)."""
         dA = A if isinstance(A, DeviceCsr) else DeviceCsr(self, A)
@@ -256,6 +312,13 @@ class DeviceExecutor:
             self.close()
         except Exception:
             pass
+
+
+def nccl_unique_id() -> bytes:
+    """ncclUniqueId (128 bytes) for DeviceExecutor(world > 1); create on rank 0."""
+    buf = C.create_string_buffer(128)
+    _check(capi.lib().pgm_nccl_unique_id(buf))
+    return buf.raw
 
 
 class DeviceCsr:
