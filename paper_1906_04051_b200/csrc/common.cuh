@@ -14,7 +14,7 @@ constexpr int SPMV_THREADS = 256;
 constexpr int SPMV_UNROLL = 8;
 constexpr int SW_THREADS = 128;       // sweep block: one row per thread
 constexpr int CH = SW_THREADS;        // rows per sweep chunk
-constexpr int GROUP = 16;             // first-level reduction group (blocks)
+constexpr int GROUP = 32;             // first-level reduction group (blocks, one per lane)
 constexpr int MAX_M = 112;            // Ritz harvest keeps [H | H^-1] in smem
 constexpr int MAX_R1 = 32;            // r_max + 1 bound of the register fast path
 constexpr int RITZ_THREADS = 256;
@@ -89,20 +89,16 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// acc: [nv][32] per-lane accumulators in smem (each value owned by one warp).
-// Every block writes its block sums; the last block of every GROUP sums its
-// group in block order; the last group-reducer sums the groups in order and
-// returns true with red[0..nv) filled.  The summation order depends only on
-// the grid size, so results are identical run to run.
-__device__ __forceinline__ bool grid_reduce(const double* acc, int nv, const Params& P,
+// bvals: the block's nv sums (smem).  Every block writes them; the last block
+// of every GROUP sums its group in block order; the last group-reducer sums
+// the groups in order and returns true with red[0..nv) filled.  The summation
+// order depends only on the grid size, so results are identical run to run.
+__device__ __forceinline__ bool grid_reduce(const double* bvals, int nv, const Params& P,
                                             double* red) {
   __shared__ int s_flag;
   const int G = gridDim.x, NG = (G + GROUP - 1) / GROUP;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int v = warp; v < nv; v += nw) {
-    const double s = warp_sum(acc[v * 32 + lane]);
-    if (lane == 0) P.part[(size_t)v * G + blockIdx.x] = s;
-  }
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) P.part[(size_t)v * G + blockIdx.x] = bvals[v];
   __threadfence();
   __syncthreads();
   const int grp = blockIdx.x / GROUP;
@@ -115,10 +111,11 @@ __device__ __forceinline__ bool grid_reduce(const double* acc, int nv, const Par
   __syncthreads();
   if (!s_flag) return false;
   __threadfence();
-  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-    double s = 0.0;
-    for (int bb = g0; bb < g0 + gsize; ++bb) s += __ldcg(&P.part[(size_t)v * G + bb]);
-    P.gpart[(size_t)v * NG + grp] = s;
+  // level 1: one warp per value, lane = block of the group
+  for (int v = warp; v < nv; v += nw) {
+    double s = lane < gsize ? __ldcg(&P.part[(size_t)v * G + g0 + lane]) : 0.0;
+    s = warp_sum(s);
+    if (lane == 0) P.gpart[(size_t)v * NG + grp] = s;
   }
   if (threadIdx.x == 0) P.cnt[1 + grp] = 0;
   __threadfence();
@@ -130,10 +127,12 @@ __device__ __forceinline__ bool grid_reduce(const double* acc, int nv, const Par
   __syncthreads();
   if (!s_flag) return false;
   __threadfence();
-  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+  // level 2: one warp per value, lanes stride over the groups
+  for (int v = warp; v < nv; v += nw) {
     double s = 0.0;
-    for (int q = 0; q < NG; ++q) s += __ldcg(&P.gpart[(size_t)v * NG + q]);
-    red[v] = s;
+    for (int q = lane; q < NG; q += 32) s += __ldcg(&P.gpart[(size_t)v * NG + q]);
+    s = warp_sum(s);
+    if (lane == 0) red[v] = s;
   }
   if (threadIdx.x == 0) P.cnt[0] = 0;
   __syncthreads();

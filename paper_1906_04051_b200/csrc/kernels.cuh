@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "finish.cuh"
+#include "tma.cuh"
 
 namespace pgm {
 
@@ -33,42 +34,155 @@ struct Sell {
   int n;
 };
 
+// Slice layout: entry (lane, t) of a slice lives at base + (t/4)*128 + lane*4 + t%4,
+// so each lane reads 4 consecutive column ids (one uint4) and 4 values (two
+// double2) per group: every warp load instruction moves a contiguous 512 B or
+// 1 KB block.  Slice lengths are padded to a multiple of 4.
 __device__ __forceinline__ void spmv_tile(const Sell& A, const double* __restrict__ x, int tile,
                                           double* ys) {
+  constexpr int UG = SPMV_UNROLL / 4;  // 4-entry groups in flight per lane
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
   for (int sl = warp; sl < SPT; sl += nw) {
     const size_t s = (size_t)tile * SPT + sl;
     const unsigned long long base = A.sptr[s];
-    const int L = (int)((A.sptr[s + 1] - base) >> 5);
-    if (L == 0) continue;
+    const int L4 = (int)((A.sptr[s + 1] - base) >> 7);
+    if (L4 == 0) continue;
     const int len = (int)A.lane_len[s * 32 + lane];
     const unsigned short ro = A.lane_row[s * 32 + lane];
-    const double* vp = A.val + base + lane;
-    const unsigned* cp = A.col + base + lane;
+    const uint4* cp = reinterpret_cast<const uint4*>(A.col + base) + lane;
+    const double2* vp = reinterpret_cast<const double2*>(A.val + base) + 2 * lane;
     double acc = 0.0;
-    for (int t = 0; t < L; t += SPMV_UNROLL) {
-      double v[SPMV_UNROLL];
-      unsigned c[SPMV_UNROLL];
+    // software pipeline: the streaming loads of group g+UG are in flight while
+    // the x gathers and the accumulation of group g run
+    uint4 c[UG];
+    double2 va[UG], vb[UG];
 #pragma unroll
-      for (int u = 0; u < SPMV_UNROLL; ++u) {
-        if (t + u < L) {
-          v[u] = __ldcs(vp + (size_t)(t + u) * 32);
-          c[u] = __ldcs(cp + (size_t)(t + u) * 32);
+    for (int u = 0; u < UG; ++u) {
+      if (u < L4) {
+        c[u] = __ldcs(cp + (size_t)u * 32);
+        va[u] = __ldcs(vp + (size_t)u * 64);
+        vb[u] = __ldcs(vp + (size_t)u * 64 + 1);
+      }
+    }
+    for (int g = 0; g < L4; g += UG) {
+      uint4 cn[UG];
+      double2 van[UG], vbn[UG];
+#pragma unroll
+      for (int u = 0; u < UG; ++u) {
+        if (g + UG + u < L4) {
+          cn[u] = __ldcs(cp + (size_t)(g + UG + u) * 32);
+          van[u] = __ldcs(vp + (size_t)(g + UG + u) * 64);
+          vbn[u] = __ldcs(vp + (size_t)(g + UG + u) * 64 + 1);
         }
       }
-      double xv[SPMV_UNROLL];
+      double xv[UG][4];
 #pragma unroll
-      for (int u = 0; u < SPMV_UNROLL; ++u) xv[u] = (t + u < len) ? __ldg(x + c[u]) : 0.0;
+      for (int u = 0; u < UG; ++u) {
+        const int t = (g + u) * 4;
+        xv[u][0] = (t + 0 < len) ? __ldg(x + c[u].x) : 0.0;
+        xv[u][1] = (t + 1 < len) ? __ldg(x + c[u].y) : 0.0;
+        xv[u][2] = (t + 2 < len) ? __ldg(x + c[u].z) : 0.0;
+        xv[u][3] = (t + 3 < len) ? __ldg(x + c[u].w) : 0.0;
+      }
 #pragma unroll
-      for (int u = 0; u < SPMV_UNROLL; ++u)
-        if (t + u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+      for (int u = 0; u < UG; ++u) {
+        const int t = (g + u) * 4;
+        if (t + 0 < len) acc = __dadd_rn(acc, __dmul_rn(va[u].x, xv[u][0]));
+        if (t + 1 < len) acc = __dadd_rn(acc, __dmul_rn(va[u].y, xv[u][1]));
+        if (t + 2 < len) acc = __dadd_rn(acc, __dmul_rn(vb[u].x, xv[u][2]));
+        if (t + 3 < len) acc = __dadd_rn(acc, __dmul_rn(vb[u].y, xv[u][3]));
+      }
+#pragma unroll
+      for (int u = 0; u < UG; ++u) {
+        c[u] = cn[u];
+        va[u] = van[u];
+        vb[u] = vbn[u];
+      }
     }
     if (ro != 0xFFFF) ys[ro] = acc;
   }
 }
 
+// ---- warp-level row-chunk dot products ---------------------------------------
+// A warp owns 32 consecutive rows (lane = row).  Dot products of the row
+// values o with a set of vectors are formed 16 values at a time: every lane
+// writes its 16 products into a per-warp transposed tile tp[16][33] (smem),
+// then lane pairs (v, v+16) sum the 32 products of value v in a fixed order
+// and the lower lane keeps the running sum in register slot v / 16.
+// Deterministic (fixed order everywhere) and barrier-free (only __syncwarp).
+constexpr int TPR = 16;                 // values per batch
+constexpr int TPS = 33;                 // padded tile row (doubles)
+constexpr int TP_DOUBLES = TPR * TPS;   // per-warp tile
+constexpr int NVL = 9;                  // accumulator slots: up to 144 values
+
+__device__ __forceinline__ double tp_sum16(const double* tp, int lane) {
+  const double* p = tp + (lane & 15) * TPS + (lane >> 4) * 16;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+  for (int q = 0; q < 16; q += 4) {
+    a0 += p[q];
+    a1 += p[q + 1];
+    a2 += p[q + 2];
+    a3 += p[q + 3];
+  }
+  double s = (a0 + a1) + (a2 + a3);
+  s += __shfl_xor_sync(0xffffffffu, s, 16);
+  return s;
+}
+
+// Products for values [v0, v0 + cnt) supplied by prod(v); accumulated in slot.
+template <class F>
+__device__ __forceinline__ void tp_batch(double* tp, double& slot_acc, int v0, int cnt, int lane,
+                                         F prod) {
+  double p[TPR];
+#pragma unroll
+  for (int j = 0; j < TPR; ++j) p[j] = (j < cnt) ? prod(v0 + j) : 0.0;
+  __syncwarp();  // scheduling fence: all loads of the batch issued before the stores
+#pragma unroll
+  for (int j = 0; j < TPR; ++j)
+    if (j < cnt) tp[j * TPS + lane] = p[j];
+  __syncwarp();
+  const double s = tp_sum16(tp, lane);
+  if (lane < cnt) slot_acc += s;
+  __syncwarp();
+}
+
+// All nv values: prod(v) for v in [0, nv).
+template <class F>
+__device__ __forceinline__ void tp_all(double* tp, double (&acc)[NVL], int nv, int lane, F prod) {
+#pragma unroll
+  for (int sl = 0; sl < NVL; ++sl) {
+    const int v0 = sl * TPR;
+    if (v0 >= nv) break;
+    tp_batch(tp, acc[sl], v0, min(TPR, nv - v0), lane, prod);
+  }
+}
+
+// Block combine of the per-warp accumulators (fixed warp order) into bvals[nv].
+__device__ __forceinline__ void warps_to_block(const double (&acc)[NVL], int nv, double* wacc,
+                                               double* bvals) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (lane < TPR) {
+#pragma unroll
+    for (int sl = 0; sl < NVL; ++sl) {
+      const int v = sl * TPR + lane;
+      if (v < nv) wacc[warp * (NVL * TPR) + v] = acc[sl];
+    }
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += wacc[w * (NVL * TPR) + v];
+    bvals[v] = s;
+  }
+  __syncthreads();
+}
+
 // ---- SpMV epilogues ---------------------------------------------------------------
+// Each is called once per 32-row chunk of the tile by one warp: grow = global
+// own-row index of this lane's row, yv = (A x)[grow].
+
 // y = A x, nothing else (pgm_spmv).
 struct PlainEpi {
   const double* xin;
@@ -76,8 +190,9 @@ struct PlainEpi {
   __device__ bool skip(const Params&) const { return false; }
   __device__ int nvals(const Params&) const { return 0; }
   __device__ void prologue(const Params&, double*) const {}
-  __device__ void tile(const Params&, int row0, int rows, double* ys, double*, double*) const {
-    for (int i = threadIdx.x; i < rows; i += blockDim.x) y[row0 + i] = ys[i];
+  __device__ void chunk(const Params&, int grow, bool ok, double yv, double*, double (&)[NVL],
+                        const double*) const {
+    if (ok) y[grow] = yv;
   }
   __device__ void finish(const Params&, const double*) const {}
 };
@@ -93,26 +208,21 @@ struct StepEpi {
     if (threadIdx.x == 0) sm[0] = P.s[k];
     for (int l = threadIdx.x; l < P.d->r; l += blockDim.x) sm[1 + l] = P.c[l];
   }
-  __device__ void tile(const Params& P, int row0, int rows, double* ys, double* acc,
-                       double* sm) const {
+  __device__ void chunk(const Params& P, int grow, bool ok, double yv, double* tp,
+                        double (&acc)[NVL], const double* sm) const {
+    const int lane = threadIdx.x & 31;
     const int r = P.d->r;
-    const double sk = sm[0];
-    double* w = P.V + (size_t)(k + 1) * P.ld + P.lo + row0;
-    const double* au = P.AU + P.lo + row0;
-    for (int i = threadIdx.x; i < rows; i += blockDim.x) {
-      double y = sk * ys[i];
-      for (int l = 0; l < r; ++l) y += sm[1 + l] * au[(size_t)l * P.ld + i];
-      w[i] = y;
-      ys[i] = y;
+    const size_t ld = P.ld;
+    const double* own = P.V + P.lo + grow;
+    double y = 0.0;
+    if (ok) {
+      y = sm[0] * yv;
+      const double* au = P.AU + P.lo + grow;
+      for (int l = 0; l < r; ++l) y += sm[1 + l] * __ldg(au + (size_t)l * ld);
+      P.V[(size_t)(k + 1) * ld + P.lo + grow] = y;
     }
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int l = warp; l <= k; l += nw) {
-      const double* vl = P.V + (size_t)l * P.ld + P.lo + row0;
-      double a = 0.0;
-      for (int i = lane; i < rows; i += 32) a += vl[i] * ys[i];
-      acc[l * 32 + lane] += a;
-    }
+    tp_all(tp, acc, k + 1, lane,
+           [&](int v) { return ok ? __ldg(own + (size_t)v * ld) * y : 0.0; });
   }
   __device__ void finish(const Params& P, const double* red) const { fin_step_spmv(P, k, red); }
 };
@@ -123,28 +233,20 @@ struct ResidualEpi {
   __device__ bool skip(const Params& P) const { return P.g->error != 0 || (!initial && P.g->done); }
   __device__ int nvals(const Params& P) const { return 1 + P.d->r; }
   __device__ void prologue(const Params&, double*) const {}
-  __device__ void tile(const Params& P, int row0, int rows, double* ys, double* acc,
-                       double*) const {
-    double* w = P.V + P.lo + row0;
-    const double* b = P.b + P.lo + row0;
-    for (int i = threadIdx.x; i < rows; i += blockDim.x) {
-      const double rv = b[i] + (-ys[i]);  // r = b; r += -1 * (A x)   (gmres.cpp:143-145)
-      w[i] = rv;
-      ys[i] = rv;
+  __device__ void chunk(const Params& P, int grow, bool ok, double yv, double* tp,
+                        double (&acc)[NVL], const double*) const {
+    const int lane = threadIdx.x & 31;
+    double rv = 0.0;
+    if (ok) {
+      rv = P.b[P.lo + grow] + (-yv);  // r = b; r += -1 * (A x)   (gmres.cpp:143-145)
+      P.V[P.lo + grow] = rv;
     }
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int nv = 1 + P.d->r;
-    for (int v = warp; v < nv; v += nw) {
-      double a = 0.0;
-      if (v == 0) {
-        for (int i = lane; i < rows; i += 32) a += ys[i] * ys[i];
-      } else {
-        const double* ul = P.U + (size_t)(v - 1) * P.ld + P.lo + row0;
-        for (int i = lane; i < rows; i += 32) a += ul[i] * ys[i];
-      }
-      acc[v * 32 + lane] += a;
-    }
+    const double* u = P.U + P.lo + grow;
+    const size_t ld = P.ld;
+    tp_all(tp, acc, 1 + P.d->r, lane, [&](int v) {
+      if (!ok) return 0.0;
+      return v == 0 ? rv * rv : __ldg(u + (size_t)(v - 1) * ld) * rv;
+    });
   }
   __device__ void finish(const Params& P, const double* red) const {
     fin_residual(P, red, initial != 0);
@@ -158,38 +260,27 @@ struct PushEpi {
   __device__ void prologue(const Params& P, double* sm) const {
     if (threadIdx.x == 0) sm[0] = P.d->pscale;
   }
-  __device__ void tile(const Params& P, int row0, int rows, double* ys, double* acc,
-                       double* sm) const {
+  __device__ void chunk(const Params& P, int grow, bool ok, double yv, double* tp,
+                        double (&acc)[NVL], const double* sm) const {
+    const int lane = threadIdx.x & 31;
     const int j = P.d->r;
+    const size_t ld = P.ld;
     const double ps = sm[0];
-    double* us = sm + 8;  // TILE doubles
-    double* uj = P.U + (size_t)j * P.ld + P.lo + row0;
-    double* auj = P.AU + (size_t)j * P.ld + P.lo + row0;
-    const double* u = P.u + P.lo + row0;
-    for (int i = threadIdx.x; i < rows; i += blockDim.x) {
-      const double un = u[i] * ps;
-      const double an = ys[i] * ps;
-      uj[i] = un;
-      auj[i] = an;
-      us[i] = un;
-      ys[i] = an;
+    double un = 0.0, an = 0.0;
+    if (ok) {
+      un = P.u[P.lo + grow] * ps;
+      an = yv * ps;
+      P.U[(size_t)j * ld + P.lo + grow] = un;
+      P.AU[(size_t)j * ld + P.lo + grow] = an;
     }
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int nv = 2 * j + 1;
-    for (int v = warp; v < nv; v += nw) {
-      double a = 0.0;
-      if (v < j) {  // U_l . AU_j
-        const double* ul = P.U + (size_t)v * P.ld + P.lo + row0;
-        for (int i = lane; i < rows; i += 32) a += ul[i] * ys[i];
-      } else if (v == j) {  // U_j . AU_j
-        for (int i = lane; i < rows; i += 32) a += us[i] * ys[i];
-      } else {  // U_j . AU_l
-        const double* al = P.AU + (size_t)(v - j - 1) * P.ld + P.lo + row0;
-        for (int i = lane; i < rows; i += 32) a += us[i] * al[i];
-      }
-      acc[v * 32 + lane] += a;
-    }
+    const double* U = P.U + P.lo + grow;
+    const double* AU = P.AU + P.lo + grow;
+    tp_all(tp, acc, 2 * j + 1, lane, [&](int v) {
+      if (!ok) return 0.0;
+      if (v < j) return __ldg(U + (size_t)v * ld) * an;   // U_l . AU_j
+      if (v == j) return un * an;                          // U_j . AU_j
+      return un * __ldg(AU + (size_t)(v - j - 1) * ld);    // U_j . AU_l
+    });
   }
   __device__ void finish(const Params& P, const double* red) const { fin_push_spmv(P, red); }
 };
@@ -213,38 +304,54 @@ __device__ __forceinline__ const double* epi_input(const Params& P, const PushEp
   return P.u;
 }
 
-constexpr int EPI_SMALL = 8 + 64;  // prologue scratch (doubles) before the tile buffers
+constexpr int EPI_SMALL = 8 + 64;  // prologue scratch (doubles)
+constexpr int SPMV_WARPS = SPMV_THREADS / 32;
 
-// dynamic smem: [small EPI_SMALL | us TILE (push only) | ys TILE | acc nv*32 | red nv]
+__host__ __device__ constexpr size_t spmv_smem_doubles(int nv) {
+  return (size_t)EPI_SMALL + TILE + (size_t)SPMV_WARPS * TP_DOUBLES +
+         (size_t)SPMV_WARPS * NVL * TPR + 2 * (size_t)nv + 2;
+}
+
+// One 512-row tile per block: SELL SpMV into smem, then every warp runs the
+// epilogue on its 64 rows (2 x 32-row chunks), then the grid reduction.
+// dynamic smem: [small | ys TILE | tp per warp | wacc | bvals nv | red nv]
 template <class Epi>
 __global__ void __launch_bounds__(SPMV_THREADS) k_spmv(Sell A, Params P, Epi E) {
   extern __shared__ double sm[];
   if (E.skip(P)) return;
   const int nv = E.nvals(P);
   double* small = sm;
-  double* ys = sm + EPI_SMALL + TILE;
-  double* acc = ys + TILE;
-  double* red = acc + nv * 32;
+  double* ys = sm + EPI_SMALL;
+  double* tp = ys + TILE + (threadIdx.x >> 5) * TP_DOUBLES;
+  double* wacc = ys + TILE + SPMV_WARPS * TP_DOUBLES;
+  double* bvals = wacc + SPMV_WARPS * NVL * TPR;
+  double* red = bvals + nv;
   E.prologue(P, small);
-  for (int i = threadIdx.x; i < nv * 32; i += blockDim.x) acc[i] = 0.0;
-  __syncthreads();
+  double acc[NVL];
+#pragma unroll
+  for (int s = 0; s < NVL; ++s) acc[s] = 0.0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* x = epi_input(P, E);
   for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
     spmv_tile(A, x, tile, ys);
     __syncthreads();
     const int row0 = tile * TILE;
     const int rows = min(TILE, A.n - row0);
-    E.tile(P, row0, rows, ys, acc, small);
+    for (int sub = warp * 32; sub < TILE; sub += SPMV_THREADS) {
+      const int i = sub + lane;
+      const bool ok = i < rows;
+      E.chunk(P, row0 + i, ok, ok ? ys[i] : 0.0, tp, acc, small);
+    }
     __syncthreads();
   }
   if (nv == 0) return;
+  warps_to_block(acc, nv, wacc, bvals);
   if (P.world > 1) {
-    if (grid_reduce(acc, nv, P, red)) {
+    if (grid_reduce(bvals, nv, P, red))
       for (int v = threadIdx.x; v < nv; v += blockDim.x) P.red_out[v] = red[v];
-    }
     return;
   }
-  if (grid_reduce(acc, nv, P, red)) {
+  if (grid_reduce(bvals, nv, P, red)) {
     if (threadIdx.x == 0) E.finish(P, red);
   }
 }
@@ -369,82 +476,134 @@ __device__ __forceinline__ void sweep_finish(const Params& P, int k, const doubl
   }
 }
 
-// dynamic smem: [a np | a2 np2 | os CH | acc nv*32 | red nv | stage np*CH]
-template <int MODE>
-__global__ void __launch_bounds__(SW_THREADS) k_sweep(Params P, int k) {
+// Streaming sweep over basis blocks: each warp owns 32-row chunks (lane =
+// row), grid-strided over all warps.  Phase 1 issues every load of the chunk
+// first (NP values held in registers), then
+//   out[row] = in[row] + sum_l a_l P_l[row] + sum_l a2_l P2_l[row];
+// phase 2 forms the dot products of out with the register-resident P set
+// (qstaged) or a second set Q through the per-warp transposed tile.
+// NP = 0 is the generic path (np > 64): P re-read from L1/L2 for the dots.
+constexpr int SW_BLOCK = 128;
+constexpr int SW_WARPS = SW_BLOCK / 32;
+
+__host__ __device__ constexpr size_t sweep_smem_doubles(int nv, int np) {
+  return (size_t)SW_WARPS * TP_DOUBLES + (size_t)SW_WARPS * NVL * TPR + 2 * (size_t)nv + 2 +
+         (size_t)np;
+}
+
+template <int MODE, int NP>
+__global__ void __launch_bounds__(SW_BLOCK) k_sweep(Params P, int k) {
   extern __shared__ double sm[];
   const SweepSpec S = sweep_spec<MODE>(P, k);
   if (S.skip) return;
   const int nv = S.nq + S.selfnorm;
   const int so = S.selfnorm;
-  double* as = sm;
-  double* a2s = as + S.np;
-  double* os = a2s + S.np2;
-  double* acc = os + CH;
-  double* red = acc + nv * 32;
-  double* st = red + nv;
-  for (int l = threadIdx.x; l < S.np; l += blockDim.x) as[l] = S.a[l];
-  for (int l = threadIdx.x; l < S.np2; l += blockDim.x) a2s[l] = S.a2[l];
-  for (int i = threadIdx.x; i < nv * 32; i += blockDim.x) acc[i] = 0.0;
-  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* tp = sm + warp * TP_DOUBLES;
+  double* wacc = sm + SW_WARPS * TP_DOUBLES;
+  double* bvals = wacc + SW_WARPS * NVL * TPR;
+  double* red = bvals + nv;
+  double* as = red + nv;
+  double acc[NVL];
+#pragma unroll
+  for (int s = 0; s < NVL; ++s) acc[s] = 0.0;
   const int n = P.n;
   const size_t ld = P.ld;
-  const int nchunks = (n + CH - 1) / CH;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
-    const int row = chunk * CH + threadIdx.x;
-    const bool ok = row < n;
-    double o = 0.0;
-    if (ok) {
-      o = S.in ? S.in[row] : 0.0;
-      const double* pv = S.Pv + row;
-#pragma unroll 8
-      for (int l = 0; l < S.np; ++l) {
-        const double v = pv[(size_t)l * ld];
-        if (S.qstaged) st[l * CH + threadIdx.x] = v;
-        o += as[l] * v;
+  const int nchunks = (n + 31) >> 5;
+  const int W = gridDim.x * SW_WARPS;
+  for (int l = threadIdx.x; l < S.np; l += blockDim.x) as[l] = S.a[l];
+  __syncthreads();
+  const int has_in = S.in != nullptr;
+  const int qg = S.qstaged ? 0 : S.nq;
+  const int nseg = has_in + S.np + S.np2 + qg;
+  // L2 prefetch (TMA engine) of every 256-byte row segment of chunk c: one per lane
+  auto prefetch = [&](int c) {
+    if (c >= nchunks) return;
+    const size_t off = (size_t)c * 32;
+    for (int q = lane; q < nseg; q += 32) {
+      const double* src;
+      int l = q - has_in;
+      if (l < 0) {
+        src = S.in;
+      } else if (l < S.np) {
+        src = S.Pv + (size_t)l * ld;
+      } else if ((l -= S.np) < S.np2) {
+        src = S.P2 + (size_t)l * ld;
+      } else {
+        src = S.Q + (size_t)(l - S.np2) * ld;
       }
+      tma_prefetch_l2(src + off, 256);
+    }
+  };
+  prefetch(blockIdx.x * SW_WARPS + warp);
+  for (int c = blockIdx.x * SW_WARPS + warp; c < nchunks; c += W) {
+    prefetch(c + W);
+    const int row = c * 32 + lane;
+    const bool ok = row < n;
+    double o = (ok && S.in) ? S.in[row] : 0.0;
+    double v[NP > 0 ? NP : 1];
+    if (NP > 0) {
+#pragma unroll
+      for (int l = 0; l < NP; ++l)
+        v[l] = (l < S.np && ok) ? __ldg(S.Pv + (size_t)l * ld + row) : 0.0;
+      __syncwarp();  // scheduling fence: every load is in flight before the first use
+      double o4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int l = 0; l < NP; ++l)
+        if (l < S.np) o4[l & 3] += as[l] * v[l];
+      o += (o4[0] + o4[1]) + (o4[2] + o4[3]);
+    } else {
+      for (int l0 = 0; l0 < S.np; l0 += 16) {
+        double t[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          t[j] = (l0 + j < S.np && ok) ? __ldg(S.Pv + (size_t)(l0 + j) * ld + row) : 0.0;
+        __syncwarp();
+        double o4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (l0 + j < S.np) o4[j & 3] += as[l0 + j] * t[j];
+        o += (o4[0] + o4[1]) + (o4[2] + o4[3]);
+      }
+    }
+    if (S.np2 > 0 && ok) {
       const double* p2 = S.P2 + row;
 #pragma unroll 4
-      for (int l = 0; l < S.np2; ++l) o += a2s[l] * p2[(size_t)l * ld];
-      S.out[row] = o;
-    } else if (S.qstaged) {
-      for (int l = 0; l < S.np; ++l) st[l * CH + threadIdx.x] = 0.0;
+      for (int l = 0; l < S.np2; ++l) o += __ldg(S.a2 + l) * __ldg(p2 + (size_t)l * ld);
     }
+    if (ok) S.out[row] = o;
+    else o = 0.0;
     if (nv == 0) continue;
-    os[threadIdx.x] = o;
-    __syncthreads();
-    for (int v = warp; v < nv; v += nw) {
-      double a = 0.0;
-      if (so && v == 0) {
+    if (S.qstaged && NP > 0) {
+      // products with the register-resident P set (no selfnorm in staged modes)
 #pragma unroll
-        for (int q = 0; q < CH / 32; ++q) {
-          const double t = os[lane + 32 * q];
-          a += t * t;
-        }
-      } else if (S.qstaged) {
-        const double* sl = st + (v - so) * CH;
+      for (int sl = 0; sl < (NP + TPR - 1) / TPR; ++sl) {
+        if (sl * TPR >= nv) break;
+        const int cnt = min(TPR, nv - sl * TPR);
 #pragma unroll
-        for (int q = 0; q < CH / 32; ++q) a += sl[lane + 32 * q] * os[lane + 32 * q];
-      } else {
-        const double* ql = S.Q + (size_t)(v - so) * ld + chunk * CH;
-#pragma unroll
-        for (int q = 0; q < CH / 32; ++q) {
-          const int rr = lane + 32 * q;
-          if (chunk * CH + rr < n) a += ql[rr] * os[rr];
-        }
+        for (int j = 0; j < TPR; ++j)
+          if (j < cnt && sl * TPR + j < NP) tp[j * TPS + lane] = v[sl * TPR + j < NP ? sl * TPR + j : 0] * o;
+        __syncwarp();
+        const double s = tp_sum16(tp, lane);
+        if (lane < cnt) acc[sl] += s;
+        __syncwarp();
       }
-      acc[v * 32 + lane] += a;
+    } else {
+      const double* q = (S.qstaged ? S.Pv : S.Q) + row;
+      tp_all(tp, acc, nv, lane, [&](int vv) {
+        if (!ok) return 0.0;
+        return (so && vv == 0) ? o * o : __ldg(q + (size_t)(vv - so) * ld) * o;
+      });
     }
-    __syncthreads();
   }
   if (nv == 0) return;
+  warps_to_block(acc, nv, wacc, bvals);
   if (P.world > 1) {
-    if (grid_reduce(acc, nv, P, red))
-      for (int v = threadIdx.x; v < nv; v += blockDim.x) P.red_out[v] = red[v];
+    if (grid_reduce(bvals, nv, P, red))
+      for (int vv = threadIdx.x; vv < nv; vv += blockDim.x) P.red_out[vv] = red[vv];
     return;
   }
-  if (grid_reduce(acc, nv, P, red)) {
+  if (grid_reduce(bvals, nv, P, red)) {
     if (threadIdx.x == 0) sweep_finish<MODE>(P, k, red);
   }
 }
@@ -756,7 +915,7 @@ __global__ void k_csr_to_sell(Sell A, double* val, unsigned* col, const unsigned
   const size_t row = tile * TILE + ro;
   const size_t start = (ro != 0xFFFF) ? rp[row] : 0;
   for (int t = 0; t < L; ++t) {
-    const size_t idx = base + (size_t)t * 32 + lane;
+    const size_t idx = base + (size_t)(t >> 2) * 128 + lane * 4 + (t & 3);
     if (t < len) {
       val[idx] = v[start + t];
       if (write_cols) col[idx] = ci[start + t] - col_shift;

@@ -173,7 +173,7 @@ int occupancy(K kernel, int threads, size_t smem) {
   return std::max(1, nb);
 }
 
-constexpr int MAX_BLOCKS_PER_SM = 4;  // bounds the grid-reduction tail
+constexpr int MAX_BLOCKS_PER_SM = 8;  // bounds the grid-reduction tail
 
 // Kernel classes of the profile (pgm_context_profile).
 enum ProfClass : uint32_t {
@@ -233,18 +233,16 @@ uint32_t prof_class_sweep() {
        : (MODE >= SW_PUSH1 && MODE <= SW_PUSH3) ? PC_PUSH : PC_OTHER;
 }
 
-size_t spmv_smem(int nv) { return sizeof(double) * (EPI_SMALL + 2 * TILE + 33 * (size_t)nv); }
-size_t sweep_smem(int np, int np2, int nv, bool staged) {
-  return sizeof(double) *
-         ((size_t)np + np2 + CH + 33 * (size_t)nv + (staged ? (size_t)np * CH : 0));
-}
+size_t spmv_smem(int nv) { return sizeof(double) * spmv_smem_doubles(nv); }
 
 template <class Epi>
 Status launch_spmv(pgm_context* ctx, const pgm_matrix* A, const Params& P, const Epi& E,
                    int nvmax, uint32_t prof_k = 0) {
   const size_t smem = spmv_smem(nvmax);
-  const int occ = std::min(MAX_BLOCKS_PER_SM, occupancy(k_spmv<Epi>, SPMV_THREADS, smem));
-  const int G = std::max(1, std::min(A->ntiles, occ * ctx->nsm));
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_spmv<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // one tile per block: the hardware scheduler balances the tiles
+  const int G = std::max(1, A->ntiles);
   ProfScope ps(ctx, prof_class_of<Epi>(), prof_k);
   k_spmv<Epi><<<G, SPMV_THREADS, smem, ctx->stream>>>(A->view(), P, E);
   ctx->launches++;
@@ -252,25 +250,35 @@ Status launch_spmv(pgm_context* ctx, const pgm_matrix* A, const Params& P, const
   return {};
 }
 
-template <int MODE>
-Status launch_sweep(pgm_context* ctx, const Params& P, int k, int np, int np2, int nv,
-                    bool staged) {
-  const size_t smem = sweep_smem(np, np2, nv, staged);
-  const int occ = std::min(MAX_BLOCKS_PER_SM, occupancy(k_sweep<MODE>, SW_THREADS, smem));
-  const int nchunks = (int)((ctx->n + CH - 1) / CH);
-  const int G = std::max(1, std::min(nchunks, occ * ctx->nsm));
+template <int MODE, int NP>
+Status launch_sweep_np(pgm_context* ctx, const Params& P, int k, int nv, int np) {
+  const size_t smem = sizeof(double) * sweep_smem_doubles(nv, np);
+  const int occ = std::min(MAX_BLOCKS_PER_SM, occupancy(k_sweep<MODE, NP>, SW_BLOCK, smem));
+  const int nchunks = (int)((ctx->n + 31) / 32);
+  const int G = std::max(1, std::min((nchunks + SW_WARPS - 1) / SW_WARPS, occ * ctx->nsm));
   ProfScope ps(ctx, prof_class_sweep<MODE>(), (uint32_t)k);
-  k_sweep<MODE><<<G, SW_THREADS, smem, ctx->stream>>>(P, k);
+  k_sweep<MODE, NP><<<G, SW_BLOCK, smem, ctx->stream>>>(P, k);
   ctx->launches++;
   CU(cudaGetLastError());
   return {};
 }
 
+// np / nv: upper bounds of the register-streamed set and of the reduced values;
+// np picks the register-resident template (0 = generic path for np > 64).
+template <int MODE>
+Status launch_sweep(pgm_context* ctx, const Params& P, int k, int np, int /*np2*/, int nv, bool) {
+  if (np <= 8) return launch_sweep_np<MODE, 8>(ctx, P, k, nv, np);
+  if (np <= 16) return launch_sweep_np<MODE, 16>(ctx, P, k, nv, np);
+  if (np <= 32) return launch_sweep_np<MODE, 32>(ctx, P, k, nv, np);
+  if (np <= 64) return launch_sweep_np<MODE, 64>(ctx, P, k, nv, np);
+  return launch_sweep_np<MODE, 0>(ctx, P, k, nv, np);
+}
+
 // ---------------------------------------------------------------------------
 // Context-owned buffers
 
-Status ensure_reduction(pgm_context* ctx, int nv) {
-  const int gmax = ctx->nsm * 8;
+Status ensure_reduction(pgm_context* ctx, int nv, int gneed = 0) {
+  const int gmax = std::max(ctx->nsm * 8, gneed);
   if (ctx->part_buf && ctx->nvmax >= nv && ctx->gmax >= gmax) return {};
   dfree(ctx->part_buf);
   dfree(ctx->gpart_buf);
@@ -482,9 +490,9 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
     StepEpi se{k};
     TRY(launch_spmv(ctx, A, P, se, m + 1, (uint32_t)k));
     TRY(finish_global<100>(ctx, P, k, k + 1));
-    TRY(launch_sweep<SW_CGS2_B>(ctx, P, k, m + 1, 0, m + 1, true));
+    TRY(launch_sweep<SW_CGS2_B>(ctx, P, k, k + 1, 0, k + 1, true));
     TRY(finish_global<SW_CGS2_B>(ctx, P, k, k + 1));
-    TRY(launch_sweep<SW_CGS2_C>(ctx, P, k, m + 1, 0, R1 + 1, false));
+    TRY(launch_sweep<SW_CGS2_C>(ctx, P, k, k + 1, 0, R1 + 1, false));
     TRY(finish_global<SW_CGS2_C>(ctx, P, k, -1));
   }
   TRY(launch_sweep<SW_XUPDATE>(ctx, P, 0, m, R1, 0, false));
@@ -574,7 +582,7 @@ Status solve_impl(pgm_context* ctx, pgm_matrix* A, pgm_deflator* dflt, const dou
   if (d->ctx != ctx) return einval("pgm_solve: deflator belongs to another context");
   const int m = (int)cfg->m;
   const int maxr = (int)cfg->max_restarts;
-  TRY(ensure_reduction(ctx, std::max(m + 1, 2 * d->R1 + 1)));
+  TRY(ensure_reduction(ctx, std::max(m + 1, 2 * d->R1 + 1), A->ntiles));
   TRY(ensure_workspace(ctx, m, maxr, std::max(d->R1, 1)));
   TRY(defl_alloc_vectors(d));
   if (harvest) {
@@ -679,7 +687,7 @@ SliceLayout build_layout(const uint32_t* rp, uint32_t n) {
         }
       }
       L.sptr[s] = off;
-      off += 32ull * Lmax;
+      off += 32ull * ((Lmax + 3) / 4 * 4);  // 4-deep interleave (uint4 / double2 loads)
     }
   }
   L.sptr[nslices] = off;
@@ -854,7 +862,8 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) 
   ctx->n = ctx->part.row_end - ctx->part.row_begin;
   ctx->lo = ctx->part.halo_lo;
   ctx->hi = ctx->part.halo_hi;
-  ctx->ld = round_up(ctx->lo + ctx->n + ctx->hi, 32);
+  // +256: bulk copies read whole 256-row chunks past the last owned row
+  ctx->ld = round_up(ctx->lo + ctx->n + ctx->hi + 256, 128);
   auto bail = [&](const Status& s) {
     pgm_status c = fail(nullptr, s);
     pgm_context_destroy(ctx);
@@ -1162,6 +1171,7 @@ pgm_status pgm_deflator_push(pgm_deflator* d, pgm_matrix* a, const double* candi
   auto run = [&]() -> Status {
     if (a->ctx != ctx) return einval("pgm_deflator_push: matrix from another context");
     TRY(ensure_min_workspace(ctx, d->R1));
+    TRY(ensure_reduction(ctx, 2 * d->R1 + 1, a->ntiles));
     TRY(defl_alloc_vectors(d));
     TRY(set_gstate_idle(ctx));
     DState before;
