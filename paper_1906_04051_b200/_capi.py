@@ -72,10 +72,11 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB):
-        raise ImportError(f"libpgmres.so not built at {LIB}; run __graft_entry__.build() "
+    path = os.environ.get("PGMRES_LIB", LIB)  # variant builds for tuning studies
+    if not os.path.exists(path):
+        raise ImportError(f"libpgmres.so not built at {path}; run __graft_entry__.build() "
                           "(there is no CPU fallback)")
-    L = C.CDLL(LIB)
+    L = C.CDLL(path)
     vp, u32, i32, dbl = C.c_void_p, C.c_uint32, C.c_int32, C.c_double
     sig = {
         "pgm_context_create": ([C.POINTER(ContextConfig), C.POINTER(vp)], C.c_int),

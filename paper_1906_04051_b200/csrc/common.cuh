@@ -11,7 +11,14 @@ namespace pgm {
 constexpr int TILE = 512;             // rows per SpMV tile (SELL sort window)
 constexpr int SPT = TILE / 32;        // 32-row slices per tile
 constexpr int SPMV_THREADS = 256;
-constexpr int SPMV_UNROLL = 8;
+#ifndef PGM_SPMV_UNROLL
+#define PGM_SPMV_UNROLL 4
+#endif
+#ifndef PGM_SPMV_MINB
+#define PGM_SPMV_MINB 3
+#endif
+constexpr int SPMV_UNROLL = PGM_SPMV_UNROLL;  // entries per lane per pipeline stage
+constexpr int SPMV_MINB = PGM_SPMV_MINB;      // min resident blocks per SM (register cap)
 constexpr int SW_THREADS = 128;       // sweep block: one row per thread
 constexpr int CH = SW_THREADS;        // rows per sweep chunk
 constexpr int GROUP = 32;             // first-level reduction group (blocks, one per lane)

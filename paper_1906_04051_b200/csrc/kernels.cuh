@@ -316,7 +316,7 @@ __host__ __device__ constexpr size_t spmv_smem_doubles(int nv) {
 // epilogue on its 64 rows (2 x 32-row chunks), then the grid reduction.
 // dynamic smem: [small | ys TILE | tp per warp | wacc | bvals nv | red nv]
 template <class Epi>
-__global__ void __launch_bounds__(SPMV_THREADS) k_spmv(Sell A, Params P, Epi E) {
+__global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params P, Epi E) {
   extern __shared__ double sm[];
   if (E.skip(P)) return;
   const int nv = E.nvals(P);
