@@ -154,8 +154,7 @@ __device__ __forceinline__ void tp_all(double* tp, double (&acc)[NVL], int nv, i
 #pragma unroll
   for (int sl = 0; sl < NVL; ++sl) {
     const int v0 = sl * TPR;
-    if (v0 >= nv) break;
-    tp_batch(tp, acc[sl], v0, min(TPR, nv - v0), lane, prod);
+    if (v0 < nv) tp_batch(tp, acc[sl], v0, min(TPR, nv - v0), lane, prod);
   }
 }
 
@@ -578,7 +577,7 @@ __global__ void __launch_bounds__(SW_BLOCK) k_sweep(Params P, int k) {
       // products with the register-resident P set (no selfnorm in staged modes)
 #pragma unroll
       for (int sl = 0; sl < (NP + TPR - 1) / TPR; ++sl) {
-        if (sl * TPR >= nv) break;
+        if (sl * TPR >= nv) continue;
         const int cnt = min(TPR, nv - sl * TPR);
 #pragma unroll
         for (int j = 0; j < TPR; ++j)
@@ -597,6 +596,102 @@ __global__ void __launch_bounds__(SW_BLOCK) k_sweep(Params P, int k) {
     }
   }
   if (nv == 0) return;
+  warps_to_block(acc, nv, wacc, bvals);
+  if (P.world > 1) {
+    if (grid_reduce(bvals, nv, P, red))
+      for (int vv = threadIdx.x; vv < nv; vv += blockDim.x) P.red_out[vv] = red[vv];
+    return;
+  }
+  if (grid_reduce(bvals, nv, P, red)) {
+    if (threadIdx.x == 0) sweep_finish<MODE>(P, k, red);
+  }
+}
+
+// Exact-size CGS2 sweeps (np = k + 1 is static per Arnoldi step, so the
+// streamed set is fully unrolled without per-element predicates).  Rows past
+// the owned range are read (padding / halo memory, always allocated) and
+// masked before any store or product.
+//   SW_CGS2_B: w1 = w + sum_l a_l W_l ; dots W_l . w1 from the register copy
+//   SW_CGS2_C: w2 = w1 + sum_l a_l W_l ; ||w2||^2 and U_l . w2
+template <int MODE, int NP>
+__global__ void __launch_bounds__(SW_BLOCK) k_cgs2(Params P, int k) {
+  static_assert(MODE == SW_CGS2_B || MODE == SW_CGS2_C, "CGS2 sweeps only");
+  extern __shared__ double sm[];
+  if (!P.g->active) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* tp = sm + warp * TP_DOUBLES;
+  double* wacc = sm + SW_WARPS * TP_DOUBLES;
+  constexpr int NVB = (MODE == SW_CGS2_B) ? NP : 0;
+  const int r = (MODE == SW_CGS2_C) ? P.d->r : 0;
+  const int nv = (MODE == SW_CGS2_B) ? NP : 1 + r;
+  double* bvals = wacc + SW_WARPS * NVL * TPR;
+  double* red = bvals + nv;
+  double* as = red + nv + ((red + nv - sm) & 1);  // 16-byte aligned coefficient copy
+  const double* coef = (MODE == SW_CGS2_B) ? P.coefA : P.coefB;
+  for (int l = threadIdx.x; l < NP + 1; l += blockDim.x) as[l] = l < NP ? coef[l] : 0.0;
+  double acc[NVL];
+#pragma unroll
+  for (int s = 0; s < NVL; ++s) acc[s] = 0.0;
+  __syncthreads();
+  const int n = P.n;
+  const size_t ld = P.ld;
+  const int nchunks = (n + 31) >> 5;
+  const int W = gridDim.x * SW_WARPS;
+  const double* V0 = P.V + P.lo;
+  double* w = P.V + (size_t)(k + 1) * ld + P.lo;
+  const double* U0 = P.U + P.lo;
+  const double2* as2 = reinterpret_cast<const double2*>(as);
+  auto prefetch = [&](int c) {
+    if (c >= nchunks) return;
+    const size_t off = (size_t)c * 32;
+    for (int q = lane; q < NP + 1 + r; q += 32) {
+      const double* src = q < NP ? V0 + (size_t)q * ld : (q == NP ? w : U0 + (size_t)(q - NP - 1) * ld);
+      tma_prefetch_l2(src + off, 256);
+    }
+  };
+  prefetch(blockIdx.x * SW_WARPS + warp);
+  for (int c = blockIdx.x * SW_WARPS + warp; c < nchunks; c += W) {
+    prefetch(c + W);
+    const int row = c * 32 + lane;
+    const bool ok = row < n;
+    double v[NP];
+    const double* pv = V0 + row;
+#pragma unroll
+    for (int l = 0; l < NP; ++l) v[l] = __ldg(pv + (size_t)l * ld);
+    const double win = w[row];
+    __syncwarp();  // scheduling fence: all loads in flight before the first use
+    double o4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int l = 0; l + 1 < NP; l += 2) {
+      const double2 a2 = as2[l >> 1];
+      o4[l & 3] += a2.x * v[l];
+      o4[(l + 1) & 3] += a2.y * v[l + 1];
+    }
+    if (NP & 1) o4[(NP - 1) & 3] += as[NP - 1] * v[NP - 1];
+    double o = win + ((o4[0] + o4[1]) + (o4[2] + o4[3]));
+    if (ok) w[row] = o;
+    else o = 0.0;
+    if (MODE == SW_CGS2_B) {
+#pragma unroll
+      for (int sl = 0; sl < (NVB + TPR - 1) / TPR; ++sl) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int cnt = (NVB - sl * TPR) < TPR ? (NVB - sl * TPR) : TPR;
+#pragma unroll
+        for (int j = 0; j < TPR; ++j)
+          if (j < cnt) tp[j * TPS + lane] = v[(sl * TPR + j) < NP ? sl * TPR + j : 0] * o;
+        __syncwarp();
+        const double s = tp_sum16(tp, lane);
+        if (lane < cnt) acc[sl] += s;
+        __syncwarp();
+      }
+    } else {
+      const double* u = U0 + row;
+      tp_all(tp, acc, 1 + r, lane, [&](int vv) {
+        return vv == 0 ? o * o : __ldg(u + (size_t)(vv - 1) * ld) * o;
+      });
+    }
+  }
   warps_to_block(acc, nv, wacc, bvals);
   if (P.world > 1) {
     if (grid_reduce(bvals, nv, P, red))

@@ -263,6 +263,38 @@ Status launch_sweep_np(pgm_context* ctx, const Params& P, int k, int nv, int np)
   return {};
 }
 
+// Exact-size CGS2 sweeps (np = k + 1, fully unrolled) for k + 1 <= CGS2_EXACT_MAX.
+constexpr int CGS2_EXACT_MAX = 64;
+
+template <int MODE, int NP>
+Status launch_cgs2_np(pgm_context* ctx, const Params& P, int k, int nv) {
+  const size_t smem =
+      sizeof(double) * (sweep_smem_doubles(nv, NP) + 4);  // + alignment of the coefficient copy
+  const int occ = std::min(MAX_BLOCKS_PER_SM, occupancy(k_cgs2<MODE, NP>, SW_BLOCK, smem));
+  const int nchunks = (int)((ctx->n + 31) / 32);
+  const int G = std::max(1, std::min((nchunks + SW_WARPS - 1) / SW_WARPS, occ * ctx->nsm));
+  ProfScope ps(ctx, prof_class_sweep<MODE>(), (uint32_t)k);
+  k_cgs2<MODE, NP><<<G, SW_BLOCK, smem, ctx->stream>>>(P, k);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return {};
+}
+
+template <int MODE, int... Is>
+Status launch_cgs2_table(pgm_context* ctx, const Params& P, int k, int nv,
+                         std::integer_sequence<int, Is...>) {
+  using Fn = Status (*)(pgm_context*, const Params&, int, int);
+  static constexpr Fn table[] = {&launch_cgs2_np<MODE, Is + 1>...};
+  return table[k](ctx, P, k, nv);
+}
+
+template <int MODE>
+Status launch_cgs2(pgm_context* ctx, const Params& P, int k, int nv) {
+  if (k + 1 <= CGS2_EXACT_MAX)
+    return launch_cgs2_table<MODE>(ctx, P, k, nv, std::make_integer_sequence<int, CGS2_EXACT_MAX>{});
+  return launch_sweep_np<MODE, 0>(ctx, P, k, nv, k + 1);
+}
+
 // np / nv: upper bounds of the register-streamed set and of the reduced values;
 // np picks the register-resident template (0 = generic path for np > 64).
 template <int MODE>
@@ -490,9 +522,9 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
     StepEpi se{k};
     TRY(launch_spmv(ctx, A, P, se, m + 1, (uint32_t)k));
     TRY(finish_global<100>(ctx, P, k, k + 1));
-    TRY(launch_sweep<SW_CGS2_B>(ctx, P, k, k + 1, 0, k + 1, true));
+    TRY(launch_cgs2<SW_CGS2_B>(ctx, P, k, k + 1));
     TRY(finish_global<SW_CGS2_B>(ctx, P, k, k + 1));
-    TRY(launch_sweep<SW_CGS2_C>(ctx, P, k, k + 1, 0, R1 + 1, false));
+    TRY(launch_cgs2<SW_CGS2_C>(ctx, P, k, R1 + 1));
     TRY(finish_global<SW_CGS2_C>(ctx, P, k, -1));
   }
   TRY(launch_sweep<SW_XUPDATE>(ctx, P, 0, m, R1, 0, false));
