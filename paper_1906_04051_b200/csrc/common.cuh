@@ -14,6 +14,9 @@ constexpr int SPMV_THREADS = 256;
 #ifndef PGM_SPMV_UNROLL
 #define PGM_SPMV_UNROLL 4
 #endif
+#ifndef PGM_SPMV_PREFETCH
+#define PGM_SPMV_PREFETCH 1
+#endif
 #ifndef PGM_SPMV_MINB
 #define PGM_SPMV_MINB 3
 #endif

@@ -48,6 +48,12 @@ __device__ __forceinline__ void spmv_tile(const Sell& A, const double* __restric
     const unsigned long long base = A.sptr[s];
     const int L4 = (int)((A.sptr[s + 1] - base) >> 7);
     if (L4 == 0) continue;
+#if PGM_SPMV_PREFETCH
+    // stream the whole slice (values + column ids) into L2 through the TMA
+    // engine; the lane loads below then mostly hit L2
+    if (lane == 0) tma_prefetch_l2(A.val + base, (uint32_t)L4 * 128u * 8u);
+    if (lane == 1) tma_prefetch_l2(A.col + base, (uint32_t)L4 * 128u * 4u);
+#endif
     const int len = (int)A.lane_len[s * 32 + lane];
     const unsigned short ro = A.lane_row[s * 32 + lane];
     const uint4* cp = reinterpret_cast<const uint4*>(A.col + base) + lane;

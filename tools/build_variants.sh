@@ -2,6 +2,7 @@
 # Build libpgmres variants for tuning studies into tools/variants/<name>/libpgmres.so
 set -e
 cd "$(dirname "$0")/.."
+rm -rf tools/variants
 mkdir -p tools/variants
 build() {
   name=$1; shift
@@ -10,10 +11,8 @@ build() {
     -Xcompiler -fPIC -shared "$@" -o tools/variants/$name/libpgmres.so \
     paper_1906_04051_b200/csrc/pgmres.cu -ldl &
 }
-build u4m2 -DPGM_SPMV_UNROLL=4 -DPGM_SPMV_MINB=2
-build u4m3 -DPGM_SPMV_UNROLL=4 -DPGM_SPMV_MINB=3
-build u4m4 -DPGM_SPMV_UNROLL=4 -DPGM_SPMV_MINB=4
-build u8m3 -DPGM_SPMV_UNROLL=8 -DPGM_SPMV_MINB=3
-build u8m4 -DPGM_SPMV_UNROLL=8 -DPGM_SPMV_MINB=4
-build u16m2 -DPGM_SPMV_UNROLL=16 -DPGM_SPMV_MINB=2
+build base
+build pf1 -DPGM_SPMV_PREFETCH=1
+build pf1m4 -DPGM_SPMV_PREFETCH=1 -DPGM_SPMV_MINB=4
+build pf1u8 -DPGM_SPMV_PREFETCH=1 -DPGM_SPMV_UNROLL=8 -DPGM_SPMV_MINB=3
 wait
