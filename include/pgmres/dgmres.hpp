@@ -1,0 +1,274 @@
+// pgmres/dgmres.hpp — header-only C++ drop-in for the reference's linear-solve
+// API (/root/reference/proj/include/dgmres/{gmres,deflation,sparse}.hpp) on top
+// of the C ABI in pgmres.h.  A caller such as newton.cpp:60-70 keeps its code:
+//
+//   reference                                   drop-in (this header)
+//   dgmres::CsrMatrix          sparse.hpp:17    pgmres::CsrMatrix (same fields)
+//   dgmres::GmresConfig        gmres.hpp:17     pgmres::GmresConfig (same fields)
+//   dgmres::GmresReport        gmres.hpp:31     pgmres::GmresReport (+ write_csv)
+//   dgmres::DeflationConfig    deflation.hpp:15 pgmres::DeflationConfig
+//   dgmres::Deflator           deflation.hpp:35 pgmres::Deflator (state on the GPU)
+//   dgmres::Executor           parallel.hpp:86  pgmres::DeviceExecutor
+//   dgmres::deflated_gmres     deflation.hpp:97 pgmres::deflated_gmres
+//   dgmres::gmres_restarted    gmres.hpp:110    pgmres::gmres_restarted (opA = CSR,
+//                                               opM = nullptr; no std::function ops)
+//
+// Errors keep the reference's exception types and messages:
+// std::invalid_argument (m = 0, r_max = 0, ...) and std::runtime_error
+// ("gmres: initial residual is not finite", "gmres: non-finite Arnoldi
+// coefficient at restart X, step Y", "gmres: singular projection in least
+// squares", ...).  Link with -lpgmres (paper_1906_04051_b200/_lib).
+#pragma once
+
+#include <cstdint>
+#include <ostream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../pgmres.h"
+
+namespace pgmres {
+
+using index_t = std::uint32_t;
+using DenseVector = std::vector<double>;
+
+struct CsrMatrix {
+  index_t n = 0;
+  std::vector<index_t> row_ptr;
+  std::vector<index_t> col_idx;
+  std::vector<double> values;
+  std::uint64_t nnz() const { return col_idx.size(); }
+};
+
+struct GmresConfig {
+  std::uint32_t m = 50;
+  std::uint32_t max_restarts = 100;
+  double rel_tol = 1e-8;
+  bool fixed_iterations = false;
+  double breakdown_scale = 1e-14;
+};
+
+struct DeflationConfig {
+  std::uint32_t r_max = 20;
+  std::uint32_t drop = 1;
+  double accept_tol = 1e-8;
+  std::uint32_t inv_power_maxit = 500;
+  double inv_power_tol = 1e-10;
+  std::uint32_t power_maxit = 200;
+};
+
+struct InnerRecord {
+  std::uint32_t restart;
+  std::uint32_t inner;
+  double monitored;
+};
+
+struct DeflationRecord {
+  std::uint32_t restart;
+  std::uint32_t r;
+  double mu;
+  double smallest_ritz;
+};
+
+struct GmresReport {
+  double beta0 = 0.0;
+  std::vector<InnerRecord> inner;
+  std::vector<double> explicit_residual;
+  std::uint32_t restarts = 0;
+  std::uint64_t total_inner = 0;
+  bool converged = false;
+  bool breakdown = false;
+  double final_relative = 0.0;
+  double solve_seconds = 0.0;  // device time of the solve
+
+  // restart,inner_step,monitored_residual,explicit_residual (gmres.cpp:117-130)
+  void write_csv(std::ostream& os) const {
+    os << "restart,inner_step,monitored_residual,explicit_residual\n";
+    const auto prec = os.precision(17);
+    for (std::size_t i = 0; i < inner.size(); ++i) {
+      const InnerRecord& rec = inner[i];
+      const bool closes = i + 1 == inner.size() || inner[i + 1].restart != rec.restart;
+      os << rec.restart << ',' << rec.inner << ',' << rec.monitored << ',';
+      if (closes && rec.restart < explicit_residual.size()) os << explicit_residual[rec.restart];
+      os << '\n';
+    }
+    os.precision(prec);
+  }
+};
+
+namespace detail {
+inline void check(pgm_status s, const pgm_context* ctx) {
+  if (s == PGM_OK) return;
+  const std::string msg = pgm_last_error(ctx);
+  if (s == PGM_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+}  // namespace detail
+
+// One GPU (one rank of the z-slab partition when world > 1).
+class DeviceExecutor {
+ public:
+  explicit DeviceExecutor(int device = 0) : device_(device) {}
+  DeviceExecutor(int device, std::uint32_t n_axis, int rank, int world, const void* nccl_id)
+      : device_(device), n_axis_(n_axis), rank_(rank), world_(world), nccl_id_(nccl_id) {}
+  ~DeviceExecutor() {
+    for (auto& c : cache_) pgm_matrix_destroy(c.mat);
+    if (ctx_) pgm_context_destroy(ctx_);
+  }
+  DeviceExecutor(const DeviceExecutor&) = delete;
+  DeviceExecutor& operator=(const DeviceExecutor&) = delete;
+
+  pgm_context* context(index_t n_global) {
+    if (!ctx_) {
+      pgm_context_config cfg{device_, rank_, world_, nccl_id_, n_axis_, n_global, 1};
+      detail::check(pgm_context_create(&cfg, &ctx_), nullptr);
+      n_global_ = n_global;
+    } else if (n_global != n_global_) {
+      throw std::invalid_argument("DeviceExecutor: matrix size changed");
+    }
+    return ctx_;
+  }
+  pgm_context* handle() const { return ctx_; }
+
+  // Upload (or refresh the values of) a host CSR matrix: the sparsity pattern is
+  // uploaded once per matrix object, later calls only move the values
+  // (Newton re-assembles values on a fixed pattern, assembly.cpp:253).
+  pgm_matrix* matrix(const CsrMatrix& A) {
+    pgm_context* ctx = context(world_ == 1 ? A.n : n_global_);
+    for (auto& c : cache_)
+      if (c.key == &A && c.nnz == A.nnz() && c.n == A.n) {
+        detail::check(pgm_matrix_update_values(c.mat, A.values.data(), 0), ctx);
+        return c.mat;
+      }
+    pgm_csr_view v{A.n, A.nnz(), A.row_ptr.data(), A.col_idx.data(), A.values.data()};
+    pgm_matrix* m = nullptr;
+    detail::check(pgm_matrix_upload(ctx, &v, 0, &m), ctx);
+    cache_.push_back({&A, A.n, A.nnz(), m});
+    return m;
+  }
+
+  void spmv(const CsrMatrix& A, const DenseVector& x, DenseVector& y) {
+    pgm_matrix* m = matrix(A);
+    y.resize(x.size());
+    detail::check(pgm_spmv(m, x.data(), y.data(), 0), ctx_);
+  }
+
+ private:
+  struct Entry {
+    const CsrMatrix* key;
+    index_t n;
+    std::uint64_t nnz;
+    pgm_matrix* mat;
+  };
+  int device_ = 0;
+  std::uint32_t n_axis_ = 0;
+  int rank_ = 0, world_ = 1;
+  const void* nccl_id_ = nullptr;
+  index_t n_global_ = 0;
+  pgm_context* ctx_ = nullptr;
+  std::vector<Entry> cache_;
+};
+
+class Deflator {
+ public:
+  explicit Deflator(DeflationConfig cfg = {}) : cfg_(cfg) {
+    if (cfg_.r_max == 0) throw std::invalid_argument("deflation: r_max must be positive");
+    if (cfg_.drop == 0) throw std::invalid_argument("deflation: drop must be positive");
+  }
+  ~Deflator() {
+    if (d_) pgm_deflator_destroy(d_);
+  }
+  Deflator(const Deflator&) = delete;
+  Deflator& operator=(const Deflator&) = delete;
+
+  std::uint32_t rank() const { return info().r; }
+  double mu() const { return info().mu; }
+  std::uint32_t skipped_updates() const { return info().skipped; }
+  void reset() {
+    if (d_) detail::check(pgm_deflator_reset(d_), ctx_);
+  }
+  std::vector<DeflationRecord> history() const {
+    const Info i = info();
+    std::vector<pgm_deflation_record> raw(i.nh);
+    if (i.nh) detail::check(pgm_deflator_history(d_, raw.data(), i.nh), ctx_);
+    std::vector<DeflationRecord> out;
+    for (const auto& r : raw) out.push_back({r.restart, r.r, r.mu, r.smallest_ritz});
+    return out;
+  }
+  // restart,r,mu,smallest_ritz (deflation.cpp:266-273)
+  void write_csv(std::ostream& os) const {
+    os << "restart,r,mu,smallest_ritz\n";
+    const auto prec = os.precision(17);
+    for (const auto& h : history())
+      os << h.restart << ',' << h.r << ',' << h.mu << ',' << h.smallest_ritz << '\n';
+    os.precision(prec);
+  }
+  pgm_deflator* bind(pgm_context* ctx) {
+    if (!d_) {
+      pgm_deflation_config c{cfg_.r_max, cfg_.drop, cfg_.accept_tol, cfg_.inv_power_maxit,
+                             cfg_.inv_power_tol, cfg_.power_maxit};
+      detail::check(pgm_deflator_create(ctx, &c, &d_), ctx);
+      ctx_ = ctx;
+    } else if (ctx != ctx_) {
+      throw std::invalid_argument("Deflator is bound to another executor");
+    }
+    return d_;
+  }
+
+ private:
+  struct Info {
+    std::uint32_t r = 0, skipped = 0, nh = 0;
+    double mu = 0.0;
+  };
+  Info info() const {
+    Info i;
+    if (d_) detail::check(pgm_deflator_info(d_, &i.r, &i.mu, &i.skipped, &i.nh), ctx_);
+    return i;
+  }
+  DeflationConfig cfg_;
+  pgm_deflator* d_ = nullptr;
+  pgm_context* ctx_ = nullptr;
+};
+
+namespace detail {
+inline GmresReport solve(const CsrMatrix& A, const DenseVector& b, DenseVector& x,
+                         const GmresConfig& cfg, Deflator* d, DeviceExecutor& ex) {
+  if (cfg.m == 0) throw std::invalid_argument("GmresWorkspace: m must be positive");
+  pgm_matrix* m = ex.matrix(A);
+  pgm_context* ctx = ex.handle();
+  pgm_deflator* dd = d ? d->bind(ctx) : nullptr;
+  pgm_gmres_config c{cfg.m, cfg.max_restarts, cfg.rel_tol, cfg.fixed_iterations ? 1 : 0,
+                     cfg.breakdown_scale};
+  x.resize(b.size());
+  pgm_report r{};
+  check(pgm_solve(ctx, m, dd, b.data(), x.data(), &c, 0, &r), ctx);
+  GmresReport out;
+  out.beta0 = r.beta0;
+  out.restarts = r.restarts;
+  out.total_inner = r.total_inner;
+  out.converged = r.converged != 0;
+  out.breakdown = r.breakdown != 0;
+  out.final_relative = r.final_relative;
+  out.solve_seconds = r.solve_seconds;
+  for (std::uint32_t i = 0; i < r.n_inner; ++i)
+    out.inner.push_back({r.inner_restart[i], r.inner_step[i], r.inner_monitored[i]});
+  out.explicit_residual.assign(r.explicit_residual, r.explicit_residual + r.restarts);
+  pgm_report_free(&r);
+  return out;
+}
+}  // namespace detail
+
+// deflation.hpp:97-98
+inline GmresReport deflated_gmres(const CsrMatrix& A, const DenseVector& b, DenseVector& x,
+                                  const GmresConfig& cfg, Deflator& d, DeviceExecutor& ex) {
+  return detail::solve(A, b, x, cfg, &d, ex);
+}
+
+// gmres.hpp:110-113 for the production pair (opA = CSR SpMV, opM = nullptr).
+inline GmresReport gmres_restarted(const CsrMatrix& A, std::nullptr_t, const DenseVector& b,
+                                   DenseVector& x, const GmresConfig& cfg, DeviceExecutor& ex) {
+  return detail::solve(A, b, x, cfg, nullptr, ex);
+}
+
+}  // namespace pgmres
