@@ -47,12 +47,15 @@ enum { PGM_DEVICE_PTRS = 1 };
 typedef struct pgm_context pgm_context;
 typedef struct pgm_matrix pgm_matrix;
 typedef struct pgm_deflator pgm_deflator;
+typedef struct pgm_loopback pgm_loopback;
 
 /* One rank of a z-slab row-block partition (parallel.cpp:50-71). */
 typedef struct {
   int32_t device;         /* CUDA ordinal this rank drives                   */
   int32_t rank, world;    /* world = 1: single GPU                           */
   const void* nccl_id;    /* 128-byte ncclUniqueId from rank 0 (world > 1)   */
+  pgm_loopback* loopback; /* instead of NCCL: in-process group of `world`    */
+                          /* contexts driven by one host thread each         */
   uint32_t n_axis;        /* node planes; plane = n_axis^2 rows (0: n/world   */
                           /* contiguous split without mesh structure)        */
   uint32_t n_global;      /* total rows                                      */
@@ -116,6 +119,11 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out);
 void pgm_context_destroy(pgm_context* ctx);
 const char* pgm_last_error(const pgm_context* ctx);
 pgm_status pgm_context_partition(const pgm_context* ctx, pgm_partition* out);
+/* In-process communicator for world > 1 without NCCL (one host thread per
+ * rank, typically all on one GPU): same kernels and partition as the NCCL
+ * path, host-staged collectives.  Used to test the multi-rank path. */
+pgm_status pgm_loopback_create(int32_t world, pgm_loopback** out);
+void pgm_loopback_destroy(pgm_loopback* g);
 /* partition_rows(mesh, p)[w] without a context (parallel.cpp:50-71). */
 pgm_status pgm_partition_rows(uint32_t n_axis, uint32_t p, uint32_t w, pgm_partition* out);
 /* Device stream the library enqueues on (cudaStream_t), for callers that

@@ -121,7 +121,7 @@ class DeviceExecutor {
 
   pgm_context* context(index_t n_global) {
     if (!ctx_) {
-      pgm_context_config cfg{device_, rank_, world_, nccl_id_, n_axis_, n_global, 1};
+      pgm_context_config cfg{device_, rank_, world_, nccl_id_, nullptr, n_axis_, n_global, 1};
       detail::check(pgm_context_create(&cfg, &ctx_), nullptr);
       n_global_ = n_global;
     } else if (n_global != n_global_) {

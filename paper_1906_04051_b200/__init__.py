@@ -6,10 +6,11 @@ solver API over that ABI.
 """
 from .dgmres import (CsrMatrix, DeflationConfig, DeflationRecord, Deflator, DeviceCsr,
                      DeviceError, DeviceExecutor, GmresConfig, GmresError, GmresReport,
-                     InnerRecord, deflated_gmres, gmres_restarted)
+                     InnerRecord, LoopbackGroup, deflated_gmres, gmres_restarted,
+                     nccl_unique_id)
 
 __all__ = [
     "CsrMatrix", "DeflationConfig", "DeflationRecord", "Deflator", "DeviceCsr", "DeviceError",
     "DeviceExecutor", "GmresConfig", "GmresError", "GmresReport", "InnerRecord",
-    "deflated_gmres", "gmres_restarted",
+    "LoopbackGroup", "deflated_gmres", "gmres_restarted", "nccl_unique_id",
 ]

@@ -13,8 +13,8 @@ PGM_DEVICE_PTRS = 1
 
 class ContextConfig(C.Structure):
     _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
-                ("nccl_id", C.c_void_p), ("n_axis", C.c_uint32), ("n_global", C.c_uint32),
-                ("deterministic", C.c_int32)]
+                ("nccl_id", C.c_void_p), ("loopback", C.c_void_p), ("n_axis", C.c_uint32),
+                ("n_global", C.c_uint32), ("deterministic", C.c_int32)]
 
 
 class Partition(C.Structure):
@@ -61,7 +61,8 @@ EXPORTS = [
     "pgm_deflator_basis", "pgm_deflator_push", "pgm_deflator_truncate",
     "pgm_deflator_observe_ritz", "pgm_deflator_apply", "pgm_solve", "pgm_report_free",
     "pgm_context_launch_count", "pgm_context_set_profiling", "pgm_context_profile",
-    "pgm_bratu_nnz", "pgm_bratu_assemble", "pgm_nccl_unique_id",
+    "pgm_bratu_nnz", "pgm_bratu_assemble", "pgm_nccl_unique_id", "pgm_loopback_create",
+    "pgm_loopback_destroy",
 ]
 
 _lib = None
@@ -111,6 +112,8 @@ def lib():
         "pgm_bratu_nnz": ([vp, u32, C.POINTER(C.c_uint64)], C.c_int),
         "pgm_bratu_assemble": ([vp, u32, dbl, vp, i32, vp, vp, vp, vp], C.c_int),
         "pgm_nccl_unique_id": ([vp], C.c_int),
+        "pgm_loopback_create": ([i32, C.POINTER(vp)], C.c_int),
+        "pgm_loopback_destroy": ([vp], None),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -73,6 +75,32 @@ size_t round_up(size_t a, size_t b) { return (a + b - 1) / b * b; }
 
 // ---------------------------------------------------------------------------
 struct pgm_deflator;
+struct pgm_context;
+
+// In-process communicator: `world` contexts driven by `world` host threads of
+// one process (normally on one GPU).  It replaces only the NCCL transport, so
+// the complete world > 1 code path (partitioned rows, halo planes, per-
+// reduction allreduce + replicated finisher) runs and is testable on one GPU.
+struct pgm_loopback {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<pgm_context*> ctx;
+  std::vector<std::vector<double>> host;  // per-rank staging of reduced values
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
 
 struct pgm_context {
   int device = 0, rank = 0, world = 1;
@@ -100,8 +128,10 @@ struct pgm_context {
   GState* h_status = nullptr;  // pinned
   pgm_deflator* dummy = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  // multi-GPU
+  // multi-GPU: NCCL (one process per GPU) or an in-process loopback group
   void* nccl = nullptr;
+  struct pgm_loopback* loop = nullptr;
+  pgm_deflator* cur_defl = nullptr;  // deflator of the running solve (halo of u)
   // optional per-launch profiling (CUDA events around every hot-path kernel)
   bool prof_on = false;
   int prof_cycle = 0;
@@ -498,12 +528,14 @@ Status set_gstate_idle(pgm_context* ctx) {
 // ---------------------------------------------------------------------------
 // Multi-GPU collectives (world > 1): allreduce of the block-reduced sums,
 // then the scalar finisher on every rank.
+enum HaloKind { HV_V = 0, HV_X = 1, HV_U = 2, HV_TMP = 3 };
 Status allreduce_red(pgm_context* ctx, int nv);
-Status halo_exchange(pgm_context* ctx, double* vec);
+Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot = 0);
 
 template <int KIND>
 Status finish_global(pgm_context* ctx, const Params& P, int k, int nv) {
   if (ctx->world == 1) return {};
+  if (nv <= 0 || nv > ctx->nvmax) return Status{PGM_ESTATE, "finish_global: bad reduction size"};
   TRY(allreduce_red(ctx, nv));
   k_finish<KIND><<<1, 32, 0, ctx->stream>>>(P, k);
   ctx->launches++;
@@ -518,14 +550,14 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
   const int m = ctx->ws_m;
   const int R1 = d->R1;
   for (int k = 0; k < m; ++k) {
-    if (ctx->world > 1) TRY(halo_exchange(ctx, ctx->V + (size_t)k * ctx->ld));
+    if (ctx->world > 1) TRY(halo_exchange(ctx, HV_V, k));
     StepEpi se{k};
     TRY(launch_spmv(ctx, A, P, se, m + 1, (uint32_t)k));
     TRY(finish_global<100>(ctx, P, k, k + 1));
     TRY(launch_cgs2<SW_CGS2_B>(ctx, P, k, k + 1));
     TRY(finish_global<SW_CGS2_B>(ctx, P, k, k + 1));
     TRY(launch_cgs2<SW_CGS2_C>(ctx, P, k, R1 + 1));
-    TRY(finish_global<SW_CGS2_C>(ctx, P, k, -1));
+    TRY(finish_global<SW_CGS2_C>(ctx, P, k, R1 + 1));
   }
   TRY(launch_sweep<SW_XUPDATE>(ctx, P, 0, m, R1, 0, false));
   if (harvest) {
@@ -539,14 +571,14 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
     ctx->launches++;
     CU(cudaGetLastError());
     TRY(launch_sweep<SW_PUSH1>(ctx, P, 1, m, 0, R1 + 1, false));
-    TRY(finish_global<SW_PUSH1>(ctx, P, 1, -1));
+    TRY(finish_global<SW_PUSH1>(ctx, P, 1, R1 + 1));
     TRY(launch_sweep<SW_PUSH2>(ctx, P, 0, R1, 0, R1, true));
-    TRY(finish_global<SW_PUSH2>(ctx, P, 0, -1));
+    TRY(finish_global<SW_PUSH2>(ctx, P, 0, R1));
     TRY(launch_sweep<SW_PUSH3>(ctx, P, 0, R1, 0, 1, false));
-    TRY(finish_global<SW_PUSH3>(ctx, P, 0, -1));
-    if (ctx->world > 1) TRY(halo_exchange(ctx, d->u));
+    TRY(finish_global<SW_PUSH3>(ctx, P, 0, 1));
+    if (ctx->world > 1) TRY(halo_exchange(ctx, HV_U));
     TRY(launch_spmv(ctx, A, P, PushEpi{}, 2 * R1 + 1));
-    TRY(finish_global<102>(ctx, P, 0, -1));
+    TRY(finish_global<102>(ctx, P, 0, 2 * R1 + 1));
     {
       ProfScope ps(ctx, PC_ROTATE, 0);
       k_rotate<true><<<ctx->nsm * 4, 256, 0, ctx->stream>>>(P);
@@ -554,9 +586,9 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
     ctx->launches++;
     CU(cudaGetLastError());
   }
-  if (ctx->world > 1) TRY(halo_exchange(ctx, ctx->x));
+  if (ctx->world > 1) TRY(halo_exchange(ctx, HV_X));
   TRY(launch_spmv(ctx, A, P, ResidualEpi{0}, R1 + 1));
-  TRY(finish_global<101>(ctx, P, 0, -1));
+  TRY(finish_global<101>(ctx, P, 0, R1 + 1));
   return {};
 }
 
@@ -634,14 +666,15 @@ Status solve_impl(pgm_context* ctx, pgm_matrix* A, pgm_deflator* dflt, const dou
   gs.breakdown_scale = cfg->breakdown_scale;
   CU(cudaMemcpyAsync(ctx->g, &gs, sizeof(GState), cudaMemcpyHostToDevice, ctx->stream));
   const Params P = make_params(ctx, d);
+  ctx->cur_defl = d;
   ctx->launches = 0;
   ctx->prof.clear();
   ctx->ev_used = 0;
   ctx->prof_cycle = -1;
   CU(cudaEventRecord(ctx->ev0, ctx->stream));
-  if (ctx->world > 1) TRY(halo_exchange(ctx, ctx->x));
+  if (ctx->world > 1) TRY(halo_exchange(ctx, HV_X));
   TRY(launch_spmv(ctx, A, P, ResidualEpi{1}, d->R1 + 1));
-  TRY(finish_global<101>(ctx, P, 1, -1));
+  TRY(finish_global<101>(ctx, P, 1, d->R1 + 1));
   TRY(read_status(ctx));
   while (!ctx->h_status->done) {
     ctx->prof_cycle = ctx->h_status->restart;
@@ -800,20 +833,68 @@ Status matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags, pgm
 namespace {
 
 Status allreduce_red(pgm_context* ctx, int nv) {
+  if (ctx->loop) {
+    pgm_loopback* L = ctx->loop;
+    CU(cudaStreamSynchronize(ctx->stream));
+    L->barrier();
+    std::vector<double>& mine = L->host[ctx->rank];
+    mine.resize((size_t)nv * L->world);
+    for (int q = 0; q < L->world; ++q)
+      CU(cudaMemcpy(mine.data() + (size_t)q * nv, L->ctx[q]->red_out, 8 * (size_t)nv,
+                    cudaMemcpyDeviceToHost));
+    L->barrier();
+    std::vector<double> sum(nv, 0.0);
+    for (int q = 0; q < L->world; ++q)  // fixed rank order: identical on every rank
+      for (int v = 0; v < nv; ++v) sum[v] += mine[(size_t)q * nv + v];
+    CU(cudaMemcpyAsync(ctx->red_out, sum.data(), 8 * (size_t)nv, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return {};
+  }
   if (!nccl_lite::available() || !ctx->nccl) return Status{PGM_ENCCL, "NCCL not initialised"};
   if (nccl_lite::allreduce_sum_f64(ctx->red_out, ctx->red_out, (size_t)nv, ctx->nccl, ctx->stream) != 0)
     return Status{PGM_ENCCL, "ncclAllReduce failed"};
   return {};
 }
 
-// Exchange the two boundary planes of `vec` with the z-neighbours: own rows
+double* halo_vec(pgm_context* ctx, HaloKind kind, int slot) {
+  switch (kind) {
+    case HV_V: return ctx->V + (size_t)slot * ctx->ld;
+    case HV_X: return ctx->x;
+    case HV_U: return ctx->cur_defl ? ctx->cur_defl->u : nullptr;
+    case HV_TMP: return ctx->tmp;
+  }
+  return nullptr;
+}
+
+// Exchange the two boundary planes of a vector with the z-neighbours: own rows
 // [0, halo) go down into the lower neighbour's halo_hi region and own rows
-// [n - halo, n) go up into the upper neighbour's halo_lo region.
-Status halo_exchange(pgm_context* ctx, double* vec) {
+// [n - halo, n) go up into the upper neighbour's halo_lo region (slabs are at
+// least two planes thick, so halos only ever come from adjacent ranks).
+Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot) {
   if (ctx->world == 1) return {};
-  if (!ctx->nccl) return Status{PGM_ENCCL, "NCCL not initialised"};
+  double* vec = halo_vec(ctx, kind, slot);
   const size_t lo = ctx->lo, hi = ctx->hi, n = ctx->n;
   const int below = ctx->rank - 1, above = ctx->rank + 1;
+  if (ctx->loop) {
+    pgm_loopback* L = ctx->loop;
+    CU(cudaStreamSynchronize(ctx->stream));
+    L->barrier();
+    if (below >= 0 && lo > 0) {
+      pgm_context* nb = L->ctx[below];
+      const double* src = halo_vec(nb, kind, slot) + nb->lo + nb->n - nb->hi;
+      CU(cudaMemcpyAsync(vec, src, 8 * lo, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    if (above < ctx->world && hi > 0) {
+      pgm_context* na = L->ctx[above];
+      const double* src = halo_vec(na, kind, slot) + na->lo;
+      CU(cudaMemcpyAsync(vec + lo + n, src, 8 * hi, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    CU(cudaStreamSynchronize(ctx->stream));
+    L->barrier();
+    return {};
+  }
+  if (!ctx->nccl) return Status{PGM_ENCCL, "NCCL not initialised"};
   if (nccl_lite::group_start() != 0) return Status{PGM_ENCCL, "ncclGroupStart failed"};
   int rc = 0;
   if (below >= 0 && lo > 0) {
@@ -886,6 +967,11 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) 
       delete ctx;
       return PGM_EINVAL;
     }
+    if (cfg->n_axis / cfg->world < 2) {  // halos (2 planes) must come from adjacent ranks
+      delete ctx;
+      g_tls_err = "pgm_context_create: every z-slab needs at least two node planes";
+      return PGM_EINVAL;
+    }
   } else {
     delete ctx;
     g_tls_err = "pgm_context_create: world > 1 needs the mesh n_axis (z-slab partition)";
@@ -923,7 +1009,13 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) 
   cudaMemset(ctx->tmp, 0, 8 * ctx->ld);
   if ((s = ensure_reduction(ctx, 2 * MAX_R1 + MAX_M + 8)).code) return bail(s);
   if ((s = set_gstate_idle(ctx)).code) return bail(s);
-  if (cfg->world > 1) {
+  if (cfg->world > 1 && cfg->loopback) {
+    pgm_loopback* L = static_cast<pgm_loopback*>(cfg->loopback);
+    if (L->world != cfg->world) return bail(Status{PGM_EINVAL, "loopback group size != world"});
+    ctx->loop = L;
+    std::lock_guard<std::mutex> lk(L->mu);
+    L->ctx[cfg->rank] = ctx;
+  } else if (cfg->world > 1) {
     if (!nccl_lite::available()) return bail(Status{PGM_ENCCL, "libnccl.so.2 not loadable"});
     if (!cfg->nccl_id) return bail(Status{PGM_EINVAL, "world > 1 needs an ncclUniqueId"});
     if (nccl_lite::comm_init_rank(&ctx->nccl, cfg->world, cfg->nccl_id, cfg->rank) != 0)
@@ -965,6 +1057,18 @@ void pgm_context_destroy(pgm_context* ctx) {
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
+
+pgm_status pgm_loopback_create(int32_t world, pgm_loopback** out) {
+  if (!out || world < 1) return PGM_EINVAL;
+  auto* L = new pgm_loopback();
+  L->world = world;
+  L->ctx.assign(world, nullptr);
+  L->host.resize(world);
+  *out = L;
+  return PGM_OK;
+}
+
+void pgm_loopback_destroy(pgm_loopback* g) { delete g; }
 
 pgm_status pgm_context_partition(const pgm_context* ctx, pgm_partition* out) {
   if (!ctx || !out) return PGM_EINVAL;
@@ -1033,7 +1137,7 @@ pgm_status pgm_spmv(pgm_matrix* a, const double* x, double* y, int32_t flags) {
   cudaSetDevice(ctx->device);
   auto run = [&]() -> Status {
     TRY(copy_in(ctx, ctx->tmp + ctx->lo, x, ctx->n, flags));
-    if (ctx->world > 1) TRY(halo_exchange(ctx, ctx->tmp));
+    if (ctx->world > 1) TRY(halo_exchange(ctx, HV_TMP));
     TRY(set_gstate_idle(ctx));
     Params P = make_params(ctx, ctx->dummy);
     PlainEpi E{ctx->tmp, ctx->b + ctx->lo};
@@ -1210,17 +1314,18 @@ pgm_status pgm_deflator_push(pgm_deflator* d, pgm_matrix* a, const double* candi
     CU(cudaMemcpy(&before, d->d, sizeof(DState), cudaMemcpyDeviceToHost));
     TRY(copy_in(ctx, d->u + ctx->lo, candidate, ctx->n, flags));
     const Params P = make_params(ctx, d);
+    ctx->cur_defl = d;
     const int R1 = d->R1;
     k_push_begin<<<1, 1, 0, ctx->stream>>>(d->d, R1);
     TRY(launch_sweep<SW_PUSH1>(ctx, P, 0, 0, 0, R1 + 1, false));
-    TRY(finish_global<SW_PUSH1>(ctx, P, 0, -1));
+    TRY(finish_global<SW_PUSH1>(ctx, P, 0, R1 + 1));
     TRY(launch_sweep<SW_PUSH2>(ctx, P, 0, R1, 0, R1, true));
-    TRY(finish_global<SW_PUSH2>(ctx, P, 0, -1));
+    TRY(finish_global<SW_PUSH2>(ctx, P, 0, R1));
     TRY(launch_sweep<SW_PUSH3>(ctx, P, 0, R1, 0, 1, false));
-    TRY(finish_global<SW_PUSH3>(ctx, P, 0, -1));
-    if (ctx->world > 1) TRY(halo_exchange(ctx, d->u));
+    TRY(finish_global<SW_PUSH3>(ctx, P, 0, 1));
+    if (ctx->world > 1) TRY(halo_exchange(ctx, HV_U));
     TRY(launch_spmv(ctx, a, P, PushEpi{}, 2 * R1 + 1));
-    TRY(finish_global<102>(ctx, P, 0, -1));
+    TRY(finish_global<102>(ctx, P, 0, 2 * R1 + 1));
     k_rotate<false><<<ctx->nsm * 4, 256, 0, ctx->stream>>>(P);
     k_clear_rotate<<<1, 1, 0, ctx->stream>>>(d->d);
     CU(cudaGetLastError());
@@ -1273,7 +1378,7 @@ pgm_status pgm_deflator_apply(pgm_deflator* d, const double* v, double* w, int32
     TRY(copy_in(ctx, d->u + ctx->lo, v, ctx->n, flags));
     const Params P = make_params(ctx, d);
     TRY(launch_sweep<SW_DOTS_U>(ctx, P, 0, 0, 0, d->R1, false));
-    TRY(finish_global<SW_DOTS_U>(ctx, P, 0, -1));
+    TRY(finish_global<SW_DOTS_U>(ctx, P, 0, d->R1));
     TRY(launch_sweep<SW_AXPY_U>(ctx, P, 0, d->R1, 0, 0, false));
     TRY(copy_out(ctx, w, d->u + ctx->lo, ctx->n, flags));
     CU(cudaStreamSynchronize(ctx->stream));
@@ -1330,13 +1435,14 @@ Status bratu_assemble(pgm_context* ctx, uint32_t n_e, double lambda, const doubl
   if (n_e == 0) return einval("build_mesh: n_e must be positive");
   if (na * na * na != ctx->n_global)
     return einval("bratu: (2 n_e + 1)^3 != context n_global");
-  static bool table_done = false;
-  if (!table_done) {
+  static std::once_flag table_once;
+  static cudaError_t table_err = cudaSuccess;
+  std::call_once(table_once, [] {
     bratu::Table t;
     bratu::build_table(t);
-    CU(cudaMemcpyToSymbol(bratu::c_tab, &t, sizeof(t)));
-    table_done = true;
-  }
+    table_err = cudaMemcpyToSymbol(bratu::c_tab, &t, sizeof(t));
+  });
+  CU(table_err);
   const uint32_t rb = ctx->part.row_begin, re = ctx->part.row_end;
   const uint64_t nnz = bratu_rows_nnz(n_e, rb, re);
   if (nnz > 0xFFFFFFFFull) return Status{PGM_EINVAL, "symbolic_pattern: nnz exceeds 32-bit offsets"};

@@ -177,10 +177,12 @@ class DeviceExecutor:
     lazily from the first matrix's size."""
 
     def __init__(self, device: int = 0, *, n_global: int | None = None, n_axis: int = 0,
-                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 loopback: "LoopbackGroup | None" = None):
         self.device, self.rank, self.world = device, rank, world
         self.n_axis = n_axis
         self._nccl_id = nccl_id
+        self._loop = loopback
         self._ctx = None
         self.n_global = n_global
         if n_global is not None:
@@ -189,12 +191,13 @@ class DeviceExecutor:
     def _create(self, n_global: int):
         L = capi.lib()
         idbuf = None
-        if self.world > 1:
+        if self.world > 1 and self._loop is None:
             if self._nccl_id is None or len(self._nccl_id) != 128:
-                raise ValueError("world > 1 needs a 128-byte ncclUniqueId")
+                raise ValueError("world > 1 needs a 128-byte ncclUniqueId or a LoopbackGroup")
             idbuf = C.create_string_buffer(bytes(self._nccl_id), 128)
         cfg = capi.ContextConfig(self.device, self.rank, self.world,
                                  C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
+                                 self._loop.handle if self._loop is not None else None,
                                  self.n_axis, int(n_global), 1)
         h = C.c_void_p()
         _check(L.pgm_context_create(C.byref(cfg), C.byref(h)))
@@ -312,6 +315,23 @@ class DeviceExecutor:
             self.close()
         except Exception:
             pass
+
+
+class LoopbackGroup:
+    """In-process communicator of `world` ranks (one host thread per rank, one
+    DeviceExecutor each, normally on the same GPU): the multi-rank code path of
+    libpgmres with host-staged collectives instead of NCCL."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        _check(capi.lib().pgm_loopback_create(int(world), C.byref(h)))
+        self.handle = h
+        self.world = world
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            capi.lib().pgm_loopback_destroy(self.handle)
+            self.handle = None
 
 
 def nccl_unique_id() -> bytes:

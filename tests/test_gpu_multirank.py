@@ -1,0 +1,111 @@
+"""GPU: the multi-rank path (z-slab rows, halo planes, per-reduction allreduce
++ replicated finisher) run as W ranks on ONE GPU through the in-process
+loopback communicator (one host thread per rank).  Only the NCCL transport is
+replaced; kernels, partition (partition_rows, parallel.cpp:50-71) and
+collective placement are the production world > 1 code."""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_1906_04051_b200 as pg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def run_ranks(world, fn):
+    grp = pg.LoopbackGroup(world)
+    out, err = {}, {}
+
+    def body(r):
+        try:
+            out[r] = fn(r, grp)
+        except Exception as e:  # noqa: BLE001
+            err[r] = e
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    if err:
+        raise next(iter(err.values()))
+    return [out[r] for r in range(world)]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multirank_spmv_bitexact(cuda, ref, world):
+    ne = 10
+    na = 2 * ne + 1
+    Ar, _ = ref.first_newton_system(ne)
+    x = np.random.default_rng(world).uniform(-1, 1, Ar.n)
+
+    def rank(r, grp):
+        ex = pg.DeviceExecutor(0, n_global=na ** 3, n_axis=na, rank=r, world=world, loopback=grp)
+        A, _ = ex.assemble_bratu(ne, 6.8, device=False)
+        p = ex.partition()
+        dA = ex.upload(A)
+        y = ex.spmv(dA, x[p["row_begin"]:p["row_end"]].copy())
+        return p, y
+
+    res = run_ranks(world, rank)
+    y = np.concatenate([yy for _, yy in res])
+    assert np.array_equal(y, ref.spmv(Ar, x))
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_multirank_deflated_cfg1(cuda, golden, world):
+    ne = 10
+    na = 2 * ne + 1
+    g = golden("cfg1_defl")
+
+    def rank(r, grp):
+        ex = pg.DeviceExecutor(0, n_global=na ** 3, n_axis=na, rank=r, world=world, loopback=grp)
+        A, b = ex.assemble_bratu(ne, 6.8, device=False)
+        d = pg.Deflator(pg.DeflationConfig(), ex)
+        x = np.zeros(ex.n_own)
+        rep = pg.deflated_gmres(A, b, x, pg.GmresConfig(m=30, rel_tol=1e-10), d, ex)
+        return rep, x, d.rank(), d.mu()
+
+    res = run_ranks(world, rank)
+    x = np.concatenate([rr[1] for rr in res])
+    rep0 = res[0][0]
+    for rep, _, rk, mu in res:  # replicated scalar state
+        assert rep.total_inner == rep0.total_inner and rk == res[0][2] and mu == res[0][3]
+        assert np.array_equal(rep.monitored, rep0.monitored)
+    b0 = float(g["beta0"])
+    assert rep0.restarts == int(g["restarts"])
+    assert abs(rep0.total_inner - int(g["total_inner"])) <= 1
+    n = min(len(rep0.monitored), len(g["monitored"]))
+    assert np.max(np.abs(rep0.monitored[:n] - g["monitored"][:n])) <= 1e-10 * b0
+    assert np.linalg.norm(x - g["x"]) <= 1e-8 * np.linalg.norm(g["x"])
+    assert res[0][2] == int(g["rank"])
+
+
+def test_multirank_truncation_run(cuda, golden):
+    ne, world = 10, 2
+    na = 2 * ne + 1
+    g = golden("ne10_m4_trunc")
+
+    def rank(r, grp):
+        ex = pg.DeviceExecutor(0, n_global=na ** 3, n_axis=na, rank=r, world=world, loopback=grp)
+        A, b = ex.assemble_bratu(ne, 6.8, device=False)
+        d = pg.Deflator(pg.DeflationConfig(), ex)
+        x = np.zeros(ex.n_own)
+        rep = pg.deflated_gmres(A, b, x, pg.GmresConfig(m=4, max_restarts=24,
+                                                        fixed_iterations=True), d, ex)
+        return rep, x, [h.r for h in d.history()], d.T_block()
+
+    res = run_ranks(world, rank)
+    x = np.concatenate([rr[1] for rr in res])
+    assert res[0][2] == list(g["hist_r"])
+    assert np.abs(res[0][3] - g["T"]).max() <= 1e-8 * np.abs(g["T"]).max()
+    assert np.linalg.norm(x - g["x"]) <= 1e-8 * np.linalg.norm(g["x"])
