@@ -18,7 +18,7 @@ constexpr int SPMV_THREADS = 256;
 #define PGM_SPMV_PREFETCH 1
 #endif
 #ifndef PGM_SPMV_MINB
-#define PGM_SPMV_MINB 3
+#define PGM_SPMV_MINB 4
 #endif
 constexpr int SPMV_UNROLL = PGM_SPMV_UNROLL;  // entries per lane per pipeline stage
 constexpr int SPMV_MINB = PGM_SPMV_MINB;      // min resident blocks per SM (register cap)

@@ -332,14 +332,17 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
   double* bvals = wacc + SPMV_WARPS * NVL * TPR;
   double* red = bvals + nv;
   E.prologue(P, small);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* x = epi_input(P, E);
+  // exactly one tile per block (grid = ntiles): the epilogue accumulators are
+  // only live after the SpMV part, which keeps the SpMV loop's registers low
+  const int tile = blockIdx.x;
+  spmv_tile(A, x, tile, ys);
+  __syncthreads();
   double acc[NVL];
 #pragma unroll
   for (int s = 0; s < NVL; ++s) acc[s] = 0.0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* x = epi_input(P, E);
-  for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
-    spmv_tile(A, x, tile, ys);
-    __syncthreads();
+  {
     const int row0 = tile * TILE;
     const int rows = min(TILE, A.n - row0);
     for (int sub = warp * 32; sub < TILE; sub += SPMV_THREADS) {
@@ -347,7 +350,6 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
       const bool ok = i < rows;
       E.chunk(P, row0 + i, ok, ok ? ys[i] : 0.0, tp, acc, small);
     }
-    __syncthreads();
   }
   if (nv == 0) return;
   warps_to_block(acc, nv, wacc, bvals);

@@ -11,8 +11,8 @@ build() {
     -Xcompiler -fPIC -shared "$@" -o tools/variants/$name/libpgmres.so \
     paper_1906_04051_b200/csrc/pgmres.cu -ldl &
 }
-build base
-build pf1 -DPGM_SPMV_PREFETCH=1
-build pf1m4 -DPGM_SPMV_PREFETCH=1 -DPGM_SPMV_MINB=4
-build pf1u8 -DPGM_SPMV_PREFETCH=1 -DPGM_SPMV_UNROLL=8 -DPGM_SPMV_MINB=3
+build m3 -DPGM_SPMV_MINB=3
+build m4 -DPGM_SPMV_MINB=4
+build m5 -DPGM_SPMV_MINB=5
+build m4u8 -DPGM_SPMV_MINB=4 -DPGM_SPMV_UNROLL=8
 wait
