@@ -92,6 +92,35 @@ struct Params {
   int world;
 };
 
+// ---- programmatic dependent launch (PDL) -------------------------------------
+// The hot-path kernels are launched with programmatic stream serialization:
+// kernel N+1 may become resident once every block of kernel N has passed
+// pdl_trigger() (end of its main loop), runs its prologue (L2 prefetch of
+// data written >= 2 kernels back, never data of kernel N), then blocks in
+// pdl_wait() until kernel N has completed and its writes are visible.  Every
+// kernel calls pdl_trigger() only after its own pdl_wait(), so "written >= 2
+// kernels back" is always complete.  Without the launch attribute both are
+// no-ops.
+#ifndef PGM_PDL_ASM
+#define PGM_PDL_ASM 1
+#endif
+#ifndef PGM_SPMV_REV
+#define PGM_SPMV_REV 0
+#endif
+#ifndef PGM_SPMV_EARLY_PF
+#define PGM_SPMV_EARLY_PF 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if PGM_PDL_ASM
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#if PGM_PDL_ASM
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 // ---- reductions ---------------------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -101,8 +130,15 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // bvals: the block's nv sums (smem).  Every block writes them; the last block
 // of every GROUP sums its group in block order; the last group-reducer sums
-// the groups in order and returns true with red[0..nv) filled.  The summation
-// order depends only on the grid size, so results are identical run to run.
+// the groups in order and returns true (in every thread of that block) with
+// red[0..nv) filled.  The summation order depends only on the grid size, so
+// results are identical run to run.  Both levels handle VPW values per warp
+// pass so that several dependent L2 round trips overlap (the tail of every
+// reduction kernel is latency-bound).
+#ifndef PGM_VPW
+#define PGM_VPW 4
+#endif
+constexpr int VPW = PGM_VPW;
 __device__ __forceinline__ bool grid_reduce(const double* bvals, int nv, const Params& P,
                                             double* red) {
   __shared__ int s_flag;
@@ -121,11 +157,21 @@ __device__ __forceinline__ bool grid_reduce(const double* bvals, int nv, const P
   __syncthreads();
   if (!s_flag) return false;
   __threadfence();
-  // level 1: one warp per value, lane = block of the group
-  for (int v = warp; v < nv; v += nw) {
-    double s = lane < gsize ? __ldcg(&P.part[(size_t)v * G + g0 + lane]) : 0.0;
-    s = warp_sum(s);
-    if (lane == 0) P.gpart[(size_t)v * NG + grp] = s;
+  // level 1: lane = block of the group, VPW values per warp pass
+  for (int v0 = warp * VPW; v0 < nv; v0 += nw * VPW) {
+    double s[VPW];
+#pragma unroll
+    for (int q = 0; q < VPW; ++q)
+      s[q] = (v0 + q < nv && lane < gsize) ? __ldcg(&P.part[(size_t)(v0 + q) * G + g0 + lane]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < VPW; ++q) s[q] = warp_sum(s[q]);
+    if (lane < VPW && v0 + lane < nv) {
+      double o = s[0];
+#pragma unroll
+      for (int q = 1; q < VPW; ++q)
+        if (lane == q) o = s[q];
+      P.gpart[(size_t)(v0 + lane) * NG + grp] = o;
+    }
   }
   if (threadIdx.x == 0) P.cnt[1 + grp] = 0;
   __threadfence();
@@ -137,12 +183,28 @@ __device__ __forceinline__ bool grid_reduce(const double* bvals, int nv, const P
   __syncthreads();
   if (!s_flag) return false;
   __threadfence();
-  // level 2: one warp per value, lanes stride over the groups
-  for (int v = warp; v < nv; v += nw) {
-    double s = 0.0;
-    for (int q = lane; q < NG; q += 32) s += __ldcg(&P.gpart[(size_t)v * NG + q]);
-    s = warp_sum(s);
-    if (lane == 0) red[v] = s;
+  // level 2: lanes stride over the groups, VPW values per warp pass
+  for (int v0 = warp * VPW; v0 < nv; v0 += nw * VPW) {
+    double s[VPW];
+#pragma unroll
+    for (int q = 0; q < VPW; ++q) s[q] = 0.0;
+    for (int g = lane; g < NG; g += 32) {
+      double t[VPW];
+#pragma unroll
+      for (int q = 0; q < VPW; ++q)
+        t[q] = v0 + q < nv ? __ldcg(&P.gpart[(size_t)(v0 + q) * NG + g]) : 0.0;
+#pragma unroll
+      for (int q = 0; q < VPW; ++q) s[q] += t[q];
+    }
+#pragma unroll
+    for (int q = 0; q < VPW; ++q) s[q] = warp_sum(s[q]);
+    if (lane < VPW && v0 + lane < nv) {
+      double o = s[0];
+#pragma unroll
+      for (int q = 1; q < VPW; ++q)
+        if (lane == q) o = s[q];
+      red[v0 + lane] = o;
+    }
   }
   if (threadIdx.x == 0) P.cnt[0] = 0;
   __syncthreads();

@@ -1,5 +1,8 @@
 // Scalar "finisher" logic run once per reduction by the last block of a
-// kernel (or by k_finish after a cross-GPU allreduce).  Each function is the
+// kernel (or by k_finish after a cross-GPU allreduce).  Every fin_* function is
+// block-collective: all threads of that block call it; loops over independent
+// entries run across the threads, the inherently serial parts (Givens chain,
+// control decisions) run on thread 0 from shared-memory copies.  Each function is the
 // restatement of the reference's host-side scalar work at that point of the
 // restart cycle; citations into /root/reference/proj.
 #pragma once
@@ -16,6 +19,17 @@ __device__ __forceinline__ void defl_coeffs(const Params& P, int r, const double
                                             double* c) {
   const double amu = fabs(P.d->mu);
   for (int i = 0; i < r; ++i) {
+    double s = 0.0;
+    for (int j = 0; j < r; ++j) s += P.Tinv[i + j * P.R1] * t[j];
+    c[i] = amu * s - t[i];
+  }
+}
+
+// Block-collective version (t must be visible to every thread of the block).
+__device__ __forceinline__ void defl_coeffs_par(const Params& P, int r, const double* t,
+                                                double* c) {
+  const double amu = fabs(P.d->mu);
+  for (int i = threadIdx.x; i < r; i += blockDim.x) {
     double s = 0.0;
     for (int j = 0; j < r; ++j) s += P.Tinv[i + j * P.R1] * t[j];
     c[i] = amu * s - t[i];
@@ -39,79 +53,91 @@ __device__ __forceinline__ void set_error(const Params& P, int code, int restart
 __device__ __forceinline__ void begin_cycle(const Params& P, int restart, double beta,
                                             const double* Ur) {
   GState* g = P.g;
-  const int m = g->m;
-  g->restart = restart;
-  g->beta_cycle = beta;
-  g->steps = 0;
-  g->lucky = 0;
-  g->active = 1;
-  P.s[0] = 1.0 / beta;
-  for (int i = 0; i <= m; ++i) P.gv[i] = 0.0;
-  P.gv[0] = beta;
+  const int m = P.m;
+  const double sc = 1.0 / beta;
+  if (threadIdx.x == 0) {
+    g->restart = restart;
+    g->beta_cycle = beta;
+    g->steps = 0;
+    g->lucky = 0;
+    g->active = 1;
+    P.s[0] = sc;
+  }
+  for (int i = threadIdx.x; i <= m; i += blockDim.x) P.gv[i] = i == 0 ? beta : 0.0;
   const int r = P.d->r;
-  for (int l = 0; l < r; ++l) P.tU[l] = Ur[l] * P.s[0];
-  defl_coeffs(P, r, P.tU, P.c);
+  for (int l = threadIdx.x; l < r; l += blockDim.x) P.tU[l] = Ur[l] * sc;
+  __syncthreads();
+  defl_coeffs_par(P, r, P.tU, P.c);
 }
 
 // After the explicit residual (gmres.cpp:142-147 + :149-157 / :191-212).
 // red[0] = ||r||^2, red[1+l] = U_l . r
 __device__ void fin_residual(const Params& P, const double* red, bool initial) {
-  GState* g = P.g;
-  const double beta = sqrt(red[0]);
-  g->beta = beta;
-  if (initial) {
-    g->beta0 = beta;
-    if (!isfinite(beta)) {
-      set_error(P, 2 /*ENONFINITE*/, -1, -1);
-      return;
-    }
-    if (beta == 0.0) {
-      g->converged = 1;
-      g->final_relative = 0.0;
-      g->done = 1;
-      return;
-    }
-    if (g->max_restarts == 0) {
-      g->done = 1;
+  __shared__ int s_begin, s_restart;
+  __shared__ double s_beta;
+  if (threadIdx.x == 0) {
+    s_begin = 0;
+    GState* g = P.g;
+    const double beta = sqrt(red[0]);
+    s_beta = beta;
+    g->beta = beta;
+    bool exit_loop = false;
+    if (initial) {
+      g->beta0 = beta;
+      if (!isfinite(beta)) {
+        set_error(P, 2 /*ENONFINITE*/, -1, -1);
+      } else if (beta == 0.0) {
+        g->converged = 1;
+        g->final_relative = 0.0;
+        g->done = 1;
+      } else if (g->max_restarts == 0) {
+        g->done = 1;
+        exit_loop = true;
+      } else {
+        s_begin = 1;
+        s_restart = 0;
+      }
     } else {
-      begin_cycle(P, 0, beta, red + 1);
-      return;
+      const int restart = g->restart;
+      P.expl[restart] = beta;
+      g->restarts = restart + 1;
+      g->total_inner += (unsigned long long)g->steps;
+      exit_loop = true;
+      if (!isfinite(beta)) {
+        set_error(P, 2, restart, -1);
+        exit_loop = false;
+      } else if (g->lucky) {
+        g->breakdown = 1;
+        g->converged = 1;
+        g->done = 1;
+      } else if (!g->fixed && beta <= g->rel_tol * g->beta0) {
+        g->converged = 1;
+        g->done = 1;
+      } else if (beta == 0.0) {
+        g->converged = 1;
+        g->done = 1;
+      } else if (restart + 1 >= g->max_restarts) {
+        g->done = 1;
+      } else {
+        s_begin = 1;
+        s_restart = restart + 1;
+        exit_loop = false;
+      }
     }
-  } else {
-    const int restart = g->restart;
-    P.expl[restart] = beta;
-    g->restarts = restart + 1;
-    g->total_inner += (unsigned long long)g->steps;
-    if (!isfinite(beta)) {
-      set_error(P, 2, restart, -1);
-      return;
-    }
-    if (g->lucky) {
-      g->breakdown = 1;
-      g->converged = 1;
-      g->done = 1;
-    } else if (!g->fixed && beta <= g->rel_tol * g->beta0) {
-      g->converged = 1;
-      g->done = 1;
-    } else if (beta == 0.0) {
-      g->converged = 1;
-      g->done = 1;
-    } else if (restart + 1 >= g->max_restarts) {
-      g->done = 1;
-    } else {
-      begin_cycle(P, restart + 1, beta, red + 1);
-      return;
+    if (exit_loop) {
+      // loop exit bookkeeping (gmres.cpp:213-216)
+      g->final_relative = g->beta0 > 0.0 ? beta / g->beta0 : 0.0;
+      if (!g->converged && !g->fixed) g->converged = beta <= g->rel_tol * g->beta0;
+      g->active = 0;
     }
   }
-  // loop exit bookkeeping (gmres.cpp:213-216)
-  g->final_relative = g->beta0 > 0.0 ? beta / g->beta0 : 0.0;
-  if (!g->converged && !g->fixed) g->converged = beta <= g->rel_tol * g->beta0;
-  g->active = 0;
+  __syncthreads();
+  if (s_begin) begin_cycle(P, s_restart, s_beta, red + 1);
 }
 
 // After sweep A (fused into the step SpMV): red[l] = W_l . w, l <= k.
 __device__ __forceinline__ void fin_step_spmv(const Params& P, int k, const double* red) {
-  for (int l = 0; l <= k; ++l) {
+  for (int l = threadIdx.x; l <= k; l += blockDim.x) {
     const double h = P.s[l] * red[l];
     P.h1[l] = h;
     P.coefA[l] = -h * P.s[l];
@@ -121,7 +147,7 @@ __device__ __forceinline__ void fin_step_spmv(const Params& P, int k, const doub
 // After CGS2 pass 2 dots: red[l] = W_l . w1.  h = h1 + h2 (gmres.cpp:50-53).
 __device__ __forceinline__ void fin_sweep_b(const Params& P, int k, const double* red) {
   const size_t col = (size_t)k * (P.m + 1);
-  for (int l = 0; l <= k; ++l) {
+  for (int l = threadIdx.x; l <= k; l += blockDim.x) {
     const double h2 = P.s[l] * red[l];
     P.coefB[l] = -h2 * P.s[l];
     const double h = P.h1[l] + h2;
@@ -130,94 +156,83 @@ __device__ __forceinline__ void fin_sweep_b(const Params& P, int k, const double
   }
 }
 
-// Back-substitution (gmres.cpp:92-107) and the x-update coefficients
-// x += M^{-1} V y = V y + U (|mu| T^{-1} U^T V y - U^T V y).
-__device__ void end_cycle(const Params& P) {
-  GState* g = P.g;
-  g->active = 0;
-  const int k = g->steps, m = g->m;
-  double* y = P.xc;  // y first, scaled in place below
-  for (int i = 0; i < k; ++i) y[i] = P.gv[i];
-  for (int i = k - 1; i >= 0; --i) {
-    const double d = P.h_rot[(size_t)i * (m + 1) + i];
-    if (d == 0.0) {
-      set_error(P, 3 /*ESINGULAR*/, g->restart, i);
-      return;
-    }
-    double s = y[i];
-    for (int j = i + 1; j < k; ++j) s -= P.h_rot[(size_t)j * (m + 1) + i] * y[j];
-    y[i] = s / d;
-  }
-  const int r = P.d->r;
-  if (r > 0) {
-    double tz[MAX_R1 * 2];
-    for (int l = 0; l < r; ++l) {
-      double s = 0.0;
-      for (int j = 0; j < k; ++j) s += y[j] * P.tU[(size_t)j * P.R1 + l];
-      tz[l] = s;
-    }
-    defl_coeffs(P, r, tz, P.cx);
-  }
-  for (int j = 0; j < k; ++j) y[j] *= P.s[j];
-}
-
 // After CGS2 pass 2 update: red[0] = ||w2||^2, red[1+l] = U_l . w2.
 // h_{k+1,k}, Givens update, records and the inner-loop exits
 // (gmres.cpp:58-90, 163-180).
 __device__ void fin_sweep_c(const Params& P, int k, const double* red) {
+  __shared__ double sH[MAX_M + 2], sC[MAX_M], sS[MAX_M];
+  __shared__ int s_go;
   GState* g = P.g;
-  const int m = g->m;
-  const double hnext = sqrt(red[0]);
+  const int m = P.m;
   const size_t col = (size_t)k * (m + 1);
-  P.h_orig[col + k + 1] = hnext;
-  P.h_rot[col + k + 1] = hnext;
-  if (!isfinite(hnext)) {
-    set_error(P, 2, g->restart, k);
-    return;
+  for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+    sH[i] = P.h_rot[col + i];
+    if (i < k) {
+      sC[i] = P.cs[i];
+      sS[i] = P.sn[i];
+    }
   }
-  P.s[k + 1] = hnext > 0.0 ? 1.0 / hnext : 0.0;
-  // apply_rotations_and_update(k)
-  double* H = P.h_rot + col;
-  for (int i = 0; i < k; ++i) {
-    const double hi = H[i], hj = H[i + 1];
-    H[i] = P.cs[i] * hi + P.sn[i] * hj;
-    H[i + 1] = -P.sn[i] * hi + P.cs[i] * hj;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_go = 0;
+    const double hnext = sqrt(red[0]);
+    sH[k + 1] = hnext;
+    P.h_orig[col + k + 1] = hnext;
+    if (!isfinite(hnext)) {
+      set_error(P, 2, g->restart, k);
+    } else {
+      P.s[k + 1] = hnext > 0.0 ? 1.0 / hnext : 0.0;
+      // apply_rotations_and_update(k)
+      for (int i = 0; i < k; ++i) {
+        const double hi = sH[i], hj = sH[i + 1];
+        sH[i] = sC[i] * hi + sS[i] * hj;
+        sH[i + 1] = -sS[i] * hi + sC[i] * hj;
+      }
+      const double a = sH[k], b = sH[k + 1];
+      const double rr = hypot(a, b);
+      double ck, sk;
+      if (rr == 0.0) {
+        ck = 1.0;
+        sk = 0.0;
+      } else {
+        ck = a / rr;
+        sk = b / rr;
+      }
+      P.cs[k] = ck;
+      P.sn[k] = sk;
+      sH[k] = rr;
+      sH[k + 1] = 0.0;
+      const double gk = P.gv[k];
+      P.gv[k + 1] = -sk * gk;
+      P.gv[k] = ck * gk;
+      const double monitored = fabs(-sk * gk);
+      const int idx = g->n_inner++;
+      P.rec_restart[idx] = (uint32_t)g->restart;
+      P.rec_step[idx] = (uint32_t)k;
+      P.rec_mon[idx] = monitored;
+      g->steps = k + 1;
+      bool stop = false;
+      if (hnext < g->breakdown_scale * g->beta_cycle) {
+        g->lucky = 1;
+        stop = true;
+      } else if (!g->fixed && monitored <= g->rel_tol * g->beta0) {
+        stop = true;
+      }
+      if (k + 1 >= m) stop = true;
+      if (stop) g->active = 0;  // back-substitution: k_end_cycle
+      s_go = !stop;
+    }
   }
-  const double a = H[k], b = H[k + 1];
-  const double rr = hypot(a, b);
-  if (rr == 0.0) {
-    P.cs[k] = 1.0;
-    P.sn[k] = 0.0;
-  } else {
-    P.cs[k] = a / rr;
-    P.sn[k] = b / rr;
+  __syncthreads();
+  for (int i = threadIdx.x; i <= k + 1; i += blockDim.x) P.h_rot[col + i] = sH[i];
+  if (s_go) {
+    const int r = P.d->r;
+    double* t = P.tU + (size_t)(k + 1) * P.R1;
+    const double sk1 = P.s[k + 1];
+    for (int l = threadIdx.x; l < r; l += blockDim.x) t[l] = red[1 + l] * sk1;
+    __syncthreads();
+    defl_coeffs_par(P, r, t, P.c);
   }
-  H[k] = rr;
-  H[k + 1] = 0.0;
-  P.gv[k + 1] = -P.sn[k] * P.gv[k];
-  P.gv[k] = P.cs[k] * P.gv[k];
-  const double monitored = fabs(P.gv[k + 1]);
-  const int idx = g->n_inner++;
-  P.rec_restart[idx] = (uint32_t)g->restart;
-  P.rec_step[idx] = (uint32_t)k;
-  P.rec_mon[idx] = monitored;
-  g->steps = k + 1;
-  bool stop = false;
-  if (hnext < g->breakdown_scale * g->beta_cycle) {
-    g->lucky = 1;
-    stop = true;
-  } else if (!g->fixed && monitored <= g->rel_tol * g->beta0) {
-    stop = true;
-  }
-  if (k + 1 >= m) stop = true;
-  if (stop) {
-    end_cycle(P);
-    return;
-  }
-  const int r = P.d->r;
-  double* t = P.tU + (size_t)(k + 1) * P.R1;
-  for (int l = 0; l < r; ++l) t[l] = red[1 + l] * P.s[k + 1];
-  defl_coeffs(P, r, t, P.c);
 }
 
 // ---- restart harvest: push_vector (deflation.cpp:123-184) ----------------------

@@ -32,6 +32,7 @@ struct Sell {
   const unsigned* col;             // local column (index into the padded x buffer)
   int ntiles;
   int n;
+  int rev;  // walk the tiles from the last one (L2 reuse of the previous kernel's tail)
 };
 
 // Slice layout: entry (lane, t) of a slice lives at base + (t/4)*128 + lane*4 + t%4,
@@ -49,10 +50,13 @@ __device__ __forceinline__ void spmv_tile(const Sell& A, const double* __restric
     const int L4 = (int)((A.sptr[s + 1] - base) >> 7);
     if (L4 == 0) continue;
 #if PGM_SPMV_PREFETCH
-    // stream the whole slice (values + column ids) into L2 through the TMA
-    // engine; the lane loads below then mostly hit L2
-    if (lane == 0) tma_prefetch_l2(A.val + base, (uint32_t)L4 * 128u * 8u);
-    if (lane == 1) tma_prefetch_l2(A.col + base, (uint32_t)L4 * 128u * 4u);
+    // stream the slice (values + column ids) into L2 through the TMA engine;
+    // the lane loads below then mostly hit L2.  The warp's first slice was
+    // prefetched ahead of the PDL wait (k_spmv).
+    if (sl != warp || !PGM_SPMV_EARLY_PF) {
+      if (lane == 0) tma_prefetch_l2(A.val + base, (uint32_t)L4 * 128u * 8u);
+      if (lane == 1) tma_prefetch_l2(A.col + base, (uint32_t)L4 * 128u * 4u);
+    }
 #endif
     const int len = (int)A.lane_len[s * 32 + lane];
     const unsigned short ro = A.lane_row[s * 32 + lane];
@@ -287,7 +291,9 @@ struct PushEpi {
       return un * __ldg(AU + (size_t)(v - j - 1) * ld);    // U_j . AU_l
     });
   }
-  __device__ void finish(const Params& P, const double* red) const { fin_push_spmv(P, red); }
+  __device__ void finish(const Params& P, const double* red) const {
+    if (threadIdx.x == 0) fin_push_spmv(P, red);
+  }
 };
 
 template <class Epi>
@@ -323,6 +329,29 @@ __host__ __device__ constexpr size_t spmv_smem_doubles(int nv) {
 template <class Epi>
 __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params P, Epi E) {
   extern __shared__ double sm[];
+#if PGM_SPMV_REV
+  const int tile = A.rev ? A.ntiles - 1 - (int)blockIdx.x : (int)blockIdx.x;
+#else
+  const int tile = (int)blockIdx.x;
+#endif
+#if PGM_SPMV_PREFETCH && PGM_SPMV_EARLY_PF
+  {
+    // L2 prefetch of this warp's first slice (values + column ids).  The
+    // matrix is never written during a solve, so this runs ahead of the PDL
+    // wait, overlapping the previous kernel's reduction tail.  (Prefetching
+    // every slice up front overflows the L2 share of the SM: slower.)
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    {
+      const int sl = w;
+      const size_t sidx = (size_t)tile * SPT + sl;
+      const unsigned long long base = A.sptr[sidx];
+      const uint32_t L4 = (uint32_t)((A.sptr[sidx + 1] - base) >> 7);
+      if (L4 > 0 && ln == 0) tma_prefetch_l2(A.val + base, L4 * 128u * 8u);
+      if (L4 > 0 && ln == 1) tma_prefetch_l2(A.col + base, L4 * 128u * 4u);
+    }
+  }
+#endif
+  pdl_wait();
   if (E.skip(P)) return;
   const int nv = E.nvals(P);
   double* small = sm;
@@ -336,7 +365,6 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
   const double* x = epi_input(P, E);
   // exactly one tile per block (grid = ntiles): the epilogue accumulators are
   // only live after the SpMV part, which keeps the SpMV loop's registers low
-  const int tile = blockIdx.x;
   spmv_tile(A, x, tile, ys);
   __syncthreads();
   double acc[NVL];
@@ -351,6 +379,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
       E.chunk(P, row0 + i, ok, ok ? ys[i] : 0.0, tp, acc, small);
     }
   }
+  pdl_trigger();
   if (nv == 0) return;
   warps_to_block(acc, nv, wacc, bvals);
   if (P.world > 1) {
@@ -358,9 +387,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
       for (int v = threadIdx.x; v < nv; v += blockDim.x) P.red_out[v] = red[v];
     return;
   }
-  if (grid_reduce(bvals, nv, P, red)) {
-    if (threadIdx.x == 0) E.finish(P, red);
-  }
+  if (grid_reduce(bvals, nv, P, red)) E.finish(P, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -472,14 +499,16 @@ __device__ __forceinline__ SweepSpec sweep_spec(const Params& P, int k) {
 
 template <int MODE>
 __device__ __forceinline__ void sweep_finish(const Params& P, int k, const double* red) {
+  // block-collective (finish.cuh); the push_vector scalars run on thread 0
   if (MODE == SW_CGS2_B) fin_sweep_b(P, k, red);
   if (MODE == SW_CGS2_C) fin_sweep_c(P, k, red);
-  if (MODE == SW_PUSH1) fin_push1(P, red);
-  if (MODE == SW_PUSH2) fin_push2(P, red);
-  if (MODE == SW_PUSH3) fin_push3(P, red);
+  if (MODE == SW_PUSH1 && threadIdx.x == 0) fin_push1(P, red);
+  if (MODE == SW_PUSH2 && threadIdx.x == 0) fin_push2(P, red);
+  if (MODE == SW_PUSH3 && threadIdx.x == 0) fin_push3(P, red);
   if (MODE == SW_DOTS_U) {
-    for (int l = 0; l < P.d->r; ++l) P.proj[l] = red[l];
-    defl_coeffs(P, P.d->r, P.proj, P.c);
+    for (int l = threadIdx.x; l < P.d->r; l += blockDim.x) P.proj[l] = red[l];
+    __syncthreads();
+    defl_coeffs_par(P, P.d->r, P.proj, P.c);
   }
 }
 
@@ -610,123 +639,261 @@ __global__ void __launch_bounds__(SW_BLOCK) k_sweep(Params P, int k) {
       for (int vv = threadIdx.x; vv < nv; vv += blockDim.x) P.red_out[vv] = red[vv];
     return;
   }
-  if (grid_reduce(bvals, nv, P, red)) {
-    if (threadIdx.x == 0) sweep_finish<MODE>(P, k, red);
+  if (grid_reduce(bvals, nv, P, red)) sweep_finish<MODE>(P, k, red);
+}
+
+// RPL consecutive rows of one vector (16-byte aligned for RPL >= 2), or zeros.
+template <int RPL>
+__device__ __forceinline__ void load_rows(const double* p, bool pred, double (&o)[RPL]) {
+  if (RPL == 1) {
+    o[0] = pred ? __ldg(p) : 0.0;
+  } else {
+#pragma unroll
+    for (int e = 0; e < RPL; e += 2) {
+      const double2 t = pred ? __ldg(reinterpret_cast<const double2*>(p + e)) : make_double2(0.0, 0.0);
+      o[e] = t.x;
+      o[e + 1] = t.y;
+    }
+  }
+}
+template <int RPL>
+__device__ __forceinline__ void store_rows(double* p, const double (&o)[RPL]) {
+  if (RPL == 1) {
+    p[0] = o[0];
+  } else {
+#pragma unroll
+    for (int e = 0; e < RPL; e += 2) *reinterpret_cast<double2*>(p + e) = make_double2(o[e], o[e + 1]);
   }
 }
 
-// Exact-size CGS2 sweeps (np = k + 1 is static per Arnoldi step, so the
-// streamed set is fully unrolled without per-element predicates).  Rows past
-// the owned range are read (padding / halo memory, always allocated) and
-// masked before any store or product.
-//   SW_CGS2_B: w1 = w + sum_l a_l W_l ; dots W_l . w1 from the register copy
-//   SW_CGS2_C: w2 = w1 + sum_l a_l W_l ; ||w2||^2 and U_l . w2
-template <int MODE, int NP>
-__global__ void __launch_bounds__(SW_BLOCK) k_cgs2(Params P, int k) {
+// CGS2 sweeps, vector set split across the warps of a block (tools/sweepbench.cu).
+//   SW_CGS2_B: w1 = w + sum_l a_l W_l ; dots W_l . w1
+//   SW_CGS2_C: w2 = w1 + sum_l b_l W_l ; ||w2||^2 and U_j . w2
+// All NW warps of a block work on the same chunk of 32*RPL rows (lane = RPL
+// consecutive rows).  Warp q streams the basis vectors l = q + NW*j (j < NPW)
+// and, in pass C, the deflation vectors U_j, j = q + NW*i, so every warp keeps
+// only a few rows in registers and the SM holds many warps' loads in flight.
+// The per-warp partial row sums meet in smem (double-buffered: one barrier
+// per chunk); the block sum of the row update is formed in warp order, and
+// each warp accumulates its own dot products in lane-private registers across
+// all of its chunks (one warp reduction at the end).  The order of every sum
+// depends only on the grid size: bitwise reproducible run to run.
+// Rows past the owned range (padding / halo memory, always allocated) are read
+// and masked before any store or product.
+// rev: walk the chunks from the end of the vectors.  Consecutive hot-path
+// kernels alternate direction, so each one starts on the rows whose basis
+// entries the previous kernel left in the 126 MB L2.
+template <int MODE, int NW, int RPL, int NPW>
+__global__ void __launch_bounds__(NW * 32) k_cgs2(Params P, int k, int rev) {
   static_assert(MODE == SW_CGS2_B || MODE == SW_CGS2_C, "CGS2 sweeps only");
-  extern __shared__ double sm[];
-  if (!P.g->active) return;
+  constexpr bool PC = MODE == SW_CGS2_C;
+  constexpr int NUW = PC ? (MAX_R1 + NW - 1) / NW : 0;
+  constexpr int NA = PC ? NUW + 1 : NPW;
+  constexpr int CR = 32 * RPL;  // rows per chunk
+  __shared__ __align__(16) double xs[2][NW][CR];
+  __shared__ double bv[NW * (NA > NPW ? NA : NPW) + 2];
+  __shared__ double redv[NW * (NA > NPW ? NA : NPW) + 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* tp = sm + warp * TP_DOUBLES;
-  double* wacc = sm + SW_WARPS * TP_DOUBLES;
-  constexpr int NVB = (MODE == SW_CGS2_B) ? NP : 0;
-  const int r = (MODE == SW_CGS2_C) ? P.d->r : 0;
-  const int nv = (MODE == SW_CGS2_B) ? NP : 1 + r;
-  double* bvals = wacc + SW_WARPS * NVL * TPR;
-  double* red = bvals + nv;
-  double* as = red + nv + ((red + nv - sm) & 1);  // 16-byte aligned coefficient copy
-  const double* coef = (MODE == SW_CGS2_B) ? P.coefA : P.coefB;
-  for (int l = threadIdx.x; l < NP + 1; l += blockDim.x) as[l] = l < NP ? coef[l] : 0.0;
-  double acc[NVL];
-#pragma unroll
-  for (int s = 0; s < NVL; ++s) acc[s] = 0.0;
-  __syncthreads();
+  const int np = k + 1;
   const int n = P.n;
   const size_t ld = P.ld;
-  const int nchunks = (n + 31) >> 5;
-  const int W = gridDim.x * SW_WARPS;
+  const int nch = (n + CR - 1) / CR;
   const double* V0 = P.V + P.lo;
+  // Ahead of the PDL wait: L2 prefetch of this warp's W_0..W_k segments of its
+  // first two chunks (W_l, l <= k, were written >= 2 kernels back).
+  for (int c = blockIdx.x; c < nch && c < (int)(blockIdx.x + 2 * gridDim.x); c += gridDim.x) {
+    const size_t off = (size_t)(rev ? nch - 1 - c : c) * CR;
+    for (int q = lane; q < NPW; q += 32) {
+      const int l = warp + NW * q;
+      if (l < np) tma_prefetch_l2(V0 + (size_t)l * ld + off, CR * 8);
+    }
+  }
+  pdl_wait();
+  if (!P.g->active) return;
+  const int r = PC ? P.d->r : 0;
   double* w = P.V + (size_t)(k + 1) * ld + P.lo;
   const double* U0 = P.U + P.lo;
-  const double2* as2 = reinterpret_cast<const double2*>(as);
+  const double* coef = PC ? P.coefB : P.coefA;
+  double aw[NPW];
+#pragma unroll
+  for (int j = 0; j < NPW; ++j) {
+    const int l = warp + NW * j;
+    aw[j] = l < np ? coef[l] : 0.0;
+  }
+  double acc[NA];
+#pragma unroll
+  for (int j = 0; j < NA; ++j) acc[j] = 0.0;
+  // L2 prefetch (TMA engine) of this warp's segments of chunk c
   auto prefetch = [&](int c) {
-    if (c >= nchunks) return;
-    const size_t off = (size_t)c * 32;
-    for (int q = lane; q < NP + 1 + r; q += 32) {
-      const double* src = q < NP ? V0 + (size_t)q * ld : (q == NP ? w : U0 + (size_t)(q - NP - 1) * ld);
-      tma_prefetch_l2(src + off, 256);
+    if (c >= nch) return;
+    const size_t off = (size_t)(rev ? nch - 1 - c : c) * CR;
+    for (int q = lane; q < NPW + NUW + 1; q += 32) {
+      const double* src = nullptr;
+      if (q < NPW) {
+        const int l = warp + NW * q;
+        if (l < np) src = V0 + (size_t)l * ld;
+      } else if (q < NPW + NUW) {
+        const int lu = warp + NW * (q - NPW);
+        if (lu < r) src = U0 + (size_t)lu * ld;
+      } else if (warp == 0) {
+        src = w;
+      }
+      if (src) tma_prefetch_l2(src + off, CR * 8);
     }
   };
-  prefetch(blockIdx.x * SW_WARPS + warp);
-  for (int c = blockIdx.x * SW_WARPS + warp; c < nchunks; c += W) {
-    prefetch(c + W);
-    const int row = c * 32 + lane;
-    const bool ok = row < n;
-    double v[NP];
-    const double* pv = V0 + row;
+  int buf = 0;
+  for (int c = blockIdx.x; c < nch; c += gridDim.x) {
+    prefetch(c + 2 * gridDim.x);
+    const int row0 = (rev ? nch - 1 - c : c) * CR + lane * RPL;
+    double v[NPW][RPL];
+    double u[NUW > 0 ? NUW : 1][RPL];
+    double win[RPL];
 #pragma unroll
-    for (int l = 0; l < NP; ++l) v[l] = __ldg(pv + (size_t)l * ld);
-    const double win = w[row];
-    __syncwarp();  // scheduling fence: all loads in flight before the first use
-    double o4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int l = 0; l + 1 < NP; l += 2) {
-      const double2 a2 = as2[l >> 1];
-      o4[l & 3] += a2.x * v[l];
-      o4[(l + 1) & 3] += a2.y * v[l + 1];
+    for (int j = 0; j < NPW; ++j) {
+      const int l = warp + NW * j;
+      load_rows<RPL>(V0 + (size_t)l * ld + row0, l < np, v[j]);
     }
-    if (NP & 1) o4[(NP - 1) & 3] += as[NP - 1] * v[NP - 1];
-    double o = win + ((o4[0] + o4[1]) + (o4[2] + o4[3]));
-    if (ok) w[row] = o;
-    else o = 0.0;
-    if (MODE == SW_CGS2_B) {
 #pragma unroll
-      for (int sl = 0; sl < (NVB + TPR - 1) / TPR; ++sl) {
-        constexpr int dummy = 0;
-        (void)dummy;
-        const int cnt = (NVB - sl * TPR) < TPR ? (NVB - sl * TPR) : TPR;
+    for (int j = 0; j < NUW; ++j) {
+      const int lu = warp + NW * j;
+      load_rows<RPL>(U0 + (size_t)lu * ld + row0, lu < r, u[j]);
+    }
+    load_rows<RPL>(w + row0, warp == 0, win);
+    __syncwarp();  // scheduling fence: every load of the chunk in flight before the first use
 #pragma unroll
-        for (int j = 0; j < TPR; ++j)
-          if (j < cnt) tp[j * TPS + lane] = v[(sl * TPR + j) < NP ? sl * TPR + j : 0] * o;
-        __syncwarp();
-        const double s = tp_sum16(tp, lane);
-        if (lane < cnt) acc[sl] += s;
-        __syncwarp();
+    for (int e = 0; e < RPL; ++e) {
+      double p0 = win[e], p1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < NPW; ++j) {
+        if (j & 1) p1 += aw[j] * v[j][e];
+        else p0 += aw[j] * v[j][e];
       }
+      xs[buf][warp][lane * RPL + e] = p0 + p1;
+    }
+    __syncthreads();
+    double o[RPL];
+#pragma unroll
+    for (int e = 0; e < RPL; ++e) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) s += xs[buf][q][lane * RPL + e];
+      o[e] = (row0 + e < n) ? s : 0.0;
+    }
+    if (warp == 0) {
+      if (row0 + RPL <= n) {
+        store_rows<RPL>(w + row0, o);
+      } else {
+#pragma unroll
+        for (int e = 0; e < RPL; ++e)
+          if (row0 + e < n) w[row0 + e] = o[e];
+      }
+    }
+    if (!PC) {
+#pragma unroll
+      for (int j = 0; j < NPW; ++j)
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) acc[j] += v[j][e] * o[e];
     } else {
-      const double* u = U0 + row;
-      tp_all(tp, acc, 1 + r, lane, [&](int vv) {
-        return vv == 0 ? o * o : __ldg(u + (size_t)(vv - 1) * ld) * o;
-      });
+#pragma unroll
+      for (int e = 0; e < RPL; ++e) {
+        if (warp == 0) acc[NUW] += o[e] * o[e];
+#pragma unroll
+        for (int j = 0; j < NUW; ++j) acc[j] += u[j][e] * o[e];
+      }
+    }
+    buf ^= 1;
+  }
+  pdl_trigger();
+  // block values: B -> bv[l] = W_l . w1 (l < np); C -> bv[0] = ||w2||^2, bv[1 + j] = U_j . w2
+  const int nv = PC ? 1 + r : np;
+#pragma unroll
+  for (int j = 0; j < NA; ++j) {
+    const double s = warp_sum(acc[j]);
+    if (lane == 0) {
+      if (!PC) {
+        const int l = warp + NW * j;
+        if (l < np) bv[l] = s;
+      } else if (j == NUW) {
+        if (warp == 0) bv[0] = s;
+      } else {
+        const int lu = warp + NW * j;
+        if (lu < r) bv[1 + lu] = s;
+      }
     }
   }
-  warps_to_block(acc, nv, wacc, bvals);
+  __syncthreads();
   if (P.world > 1) {
-    if (grid_reduce(bvals, nv, P, red))
-      for (int vv = threadIdx.x; vv < nv; vv += blockDim.x) P.red_out[vv] = red[vv];
+    if (grid_reduce(bv, nv, P, redv))
+      for (int vv = threadIdx.x; vv < nv; vv += blockDim.x) P.red_out[vv] = redv[vv];
     return;
   }
-  if (grid_reduce(bvals, nv, P, red)) {
-    if (threadIdx.x == 0) sweep_finish<MODE>(P, k, red);
-  }
+  if (grid_reduce(bv, nv, P, redv)) sweep_finish<MODE>(P, k, redv);
 }
 
 // Cross-GPU path: finisher after the allreduce of P.red_out.
 template <int KIND>
 __global__ void k_finish(Params P, int k) {
-  // KIND: 0..7 sweep modes, 100 step spmv, 101 residual (k = initial), 102 push spmv
-  if (threadIdx.x != 0) return;
+  // KIND: 0..7 sweep modes, 100 step spmv, 101 residual (k = initial), 102 push spmv.
+  // All threads of the block take part (the finishers are block-collective).
   const double* red = P.red_out;
   if (KIND == 100) {
     if (P.g->active) fin_step_spmv(P, k, red);
   } else if (KIND == 101) {
     if (!(P.g->error != 0 || (!k && P.g->done))) fin_residual(P, red, k != 0);
   } else if (KIND == 102) {
-    if (P.d->push_ok) fin_push_spmv(P, red);
+    if (P.d->push_ok && threadIdx.x == 0) fin_push_spmv(P, red);
   } else {
     const SweepSpec S = sweep_spec<KIND>(P, k);
     if (!S.skip) sweep_finish<KIND>(P, k, red);
   }
+}
+
+// End of an Arnoldi cycle (the inner loop stopped in fin_sweep_c): back-
+// substitution of the rotated Hessenberg system (solve_least_squares,
+// gmres.cpp:92-107; same row-oriented summation order, from a shared-memory
+// copy of the triangle) and the x-update coefficients
+//   x += M^{-1} V y = V y + U (|mu| T^{-1} U^T V y - U^T V y).
+// One block; dynamic smem: k*k triangle + y + tz.
+__global__ void __launch_bounds__(256) k_end_cycle(Params P) {
+  extern __shared__ double sm[];
+  __shared__ int s_ok;
+  GState* g = P.g;
+  if (g->error) return;
+  const int k = g->steps, m = P.m;
+  double* R = sm;             // k x k, column-major (upper triangle used)
+  double* y = R + k * k;      // k
+  double* tz = y + k;         // MAX_R1
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int i = e % k, j = e / k;
+    R[e] = i <= j ? P.h_rot[(size_t)j * (m + 1) + i] : 0.0;
+  }
+  for (int i = threadIdx.x; i < k; i += blockDim.x) y[i] = P.gv[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_ok = 1;
+    for (int i = k - 1; i >= 0; --i) {
+      const double d = R[i + i * k];
+      if (d == 0.0) {
+        set_error(P, 3 /*ESINGULAR*/, g->restart, i);
+        s_ok = 0;
+        break;
+      }
+      double s = y[i];
+      for (int j = i + 1; j < k; ++j) s -= R[i + j * k] * y[j];
+      y[i] = s / d;
+    }
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  const int r = P.d->r;
+  for (int l = threadIdx.x; l < r; l += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < k; ++j) s += y[j] * P.tU[(size_t)j * P.R1 + l];
+    tz[l] = s;
+  }
+  __syncthreads();
+  if (r > 0) defl_coeffs_par(P, r, tz, P.cx);
+  for (int j = threadIdx.x; j < k; j += blockDim.x) P.xc[j] = y[j] * P.s[j];
 }
 
 // ---------------------------------------------------------------------------

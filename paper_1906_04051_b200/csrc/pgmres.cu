@@ -13,6 +13,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -134,6 +135,7 @@ struct pgm_context {
   pgm_deflator* cur_defl = nullptr;  // deflator of the running solve (halo of u)
   // optional per-launch profiling (CUDA events around every hot-path kernel)
   bool prof_on = false;
+  bool pdl = true;  // programmatic dependent launch of the hot-path kernels (PGMRES_PDL=0 disables)
   int prof_cycle = 0;
   struct Rec {
     uint32_t cls, cyc, k;
@@ -166,6 +168,7 @@ struct pgm_matrix {
     S.col = col;
     S.ntiles = ntiles;
     S.n = (int)n;
+    S.rev = 0;
     return S;
   }
 };
@@ -203,7 +206,26 @@ int occupancy(K kernel, int threads, size_t smem) {
   return std::max(1, nb);
 }
 
+// Launch with programmatic stream serialization (PDL, common.cuh) when the
+// context allows it; the kernel's griddepcontrol instructions order it.
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(pgm_context* ctx, void (*kernel)(KArgs...), int grid, int block,
+                       size_t smem, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (ctx->pdl && !ctx->prof_on) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 constexpr int MAX_BLOCKS_PER_SM = 8;  // bounds the grid-reduction tail
+constexpr int MAX_SPLIT_BLOCKS_PER_SM = 32;  // warp-split CGS2 sweeps (64-128 threads)
 
 // Kernel classes of the profile (pgm_context_profile).
 enum ProfClass : uint32_t {
@@ -267,14 +289,16 @@ size_t spmv_smem(int nv) { return sizeof(double) * spmv_smem_doubles(nv); }
 
 template <class Epi>
 Status launch_spmv(pgm_context* ctx, const pgm_matrix* A, const Params& P, const Epi& E,
-                   int nvmax, uint32_t prof_k = 0) {
+                   int nvmax, uint32_t prof_k = 0, int rev = 0) {
   const size_t smem = spmv_smem(nvmax);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_spmv<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // one tile per block: the hardware scheduler balances the tiles
   const int G = std::max(1, A->ntiles);
   ProfScope ps(ctx, prof_class_of<Epi>(), prof_k);
-  k_spmv<Epi><<<G, SPMV_THREADS, smem, ctx->stream>>>(A->view(), P, E);
+  Sell sv = A->view();
+  sv.rev = rev;
+  CU(launch_pdl(ctx, k_spmv<Epi>, G, SPMV_THREADS, smem, sv, P, E));
   ctx->launches++;
   CU(cudaGetLastError());
   return {};
@@ -293,36 +317,46 @@ Status launch_sweep_np(pgm_context* ctx, const Params& P, int k, int nv, int np)
   return {};
 }
 
-// Exact-size CGS2 sweeps (np = k + 1, fully unrolled) for k + 1 <= CGS2_EXACT_MAX.
-constexpr int CGS2_EXACT_MAX = 64;
-
-template <int MODE, int NP>
-Status launch_cgs2_np(pgm_context* ctx, const Params& P, int k, int nv) {
-  const size_t smem =
-      sizeof(double) * (sweep_smem_doubles(nv, NP) + 4);  // + alignment of the coefficient copy
-  const int occ = std::min(MAX_BLOCKS_PER_SM, occupancy(k_cgs2<MODE, NP>, SW_BLOCK, smem));
-  const int nchunks = (int)((ctx->n + 31) / 32);
-  const int G = std::max(1, std::min((nchunks + SW_WARPS - 1) / SW_WARPS, occ * ctx->nsm));
+// CGS2 sweeps (np = k + 1): warp-split kernels; 4 warps per block (8 above
+// 64 vectors), 2 rows per lane (tools/sweepbench.cu, tools/run_variants.sh).
+template <int MODE, int NW, int RPL, int NPW>
+Status launch_cgs2_cfg(pgm_context* ctx, const Params& P, int k, int rev) {
+  static int occ = 0;  // per instantiation; same device geometry for every context
+  if (occ == 0) occ = std::min(MAX_SPLIT_BLOCKS_PER_SM, occupancy(k_cgs2<MODE, NW, RPL, NPW>, NW * 32, 0));
+  const int nchunks = (int)((ctx->n + 32 * RPL - 1) / (32 * RPL));
+  const int G = std::max(1, std::min(nchunks, occ * ctx->nsm));
   ProfScope ps(ctx, prof_class_sweep<MODE>(), (uint32_t)k);
-  k_cgs2<MODE, NP><<<G, SW_BLOCK, smem, ctx->stream>>>(P, k);
+  CU(launch_pdl(ctx, k_cgs2<MODE, NW, RPL, NPW>, G, NW * 32, 0, P, k, rev));
   ctx->launches++;
   CU(cudaGetLastError());
   return {};
 }
 
-template <int MODE, int... Is>
-Status launch_cgs2_table(pgm_context* ctx, const Params& P, int k, int nv,
+template <int MODE, int NW, int RPL, int... Is>
+Status launch_cgs2_table(pgm_context* ctx, const Params& P, int k, int rev, int npw,
                          std::integer_sequence<int, Is...>) {
   using Fn = Status (*)(pgm_context*, const Params&, int, int);
-  static constexpr Fn table[] = {&launch_cgs2_np<MODE, Is + 1>...};
-  return table[k](ctx, P, k, nv);
+  static constexpr Fn table[] = {&launch_cgs2_cfg<MODE, NW, RPL, Is + 1>...};
+  return table[npw - 1](ctx, P, k, rev);
 }
 
+constexpr int CGS2_SPLIT_MAX = 112;  // = MAX_M: 8 warps x 14 vectors
+
+#ifndef PGM_CGS2_RPL
+#define PGM_CGS2_RPL 2  // rows per lane (tools/run_variants.sh study: 2 beats 1)
+#endif
 template <int MODE>
-Status launch_cgs2(pgm_context* ctx, const Params& P, int k, int nv) {
-  if (k + 1 <= CGS2_EXACT_MAX)
-    return launch_cgs2_table<MODE>(ctx, P, k, nv, std::make_integer_sequence<int, CGS2_EXACT_MAX>{});
-  return launch_sweep_np<MODE, 0>(ctx, P, k, nv, k + 1);
+Status launch_cgs2(pgm_context* ctx, const Params& P, int k, int nv, int rev) {
+  constexpr int R = PGM_CGS2_RPL;
+  const int np = k + 1;
+  if (MODE == SW_CGS2_B && np <= 4) return launch_cgs2_cfg<MODE, 2, R, 2>(ctx, P, k, rev);
+  if (np <= 64)
+    return launch_cgs2_table<MODE, 4, R>(ctx, P, k, rev, (np + 3) / 4,
+                                         std::make_integer_sequence<int, 16>{});
+  if (np <= CGS2_SPLIT_MAX)
+    return launch_cgs2_table<MODE, 8, R>(ctx, P, k, rev, (np + 7) / 8,
+                                         std::make_integer_sequence<int, 14>{});
+  return launch_sweep_np<MODE, 0>(ctx, P, k, nv, np);
 }
 
 // np / nv: upper bounds of the register-streamed set and of the reduced values;
@@ -340,7 +374,7 @@ Status launch_sweep(pgm_context* ctx, const Params& P, int k, int np, int /*np2*
 // Context-owned buffers
 
 Status ensure_reduction(pgm_context* ctx, int nv, int gneed = 0) {
-  const int gmax = std::max(ctx->nsm * 8, gneed);
+  const int gmax = std::max(ctx->nsm * MAX_SPLIT_BLOCKS_PER_SM, gneed);
   if (ctx->part_buf && ctx->nvmax >= nv && ctx->gmax >= gmax) return {};
   dfree(ctx->part_buf);
   dfree(ctx->gpart_buf);
@@ -551,13 +585,24 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
   const int R1 = d->R1;
   for (int k = 0; k < m; ++k) {
     if (ctx->world > 1) TRY(halo_exchange(ctx, HV_V, k));
+    // rev = 0: alternating the walk direction per kernel (to reuse the
+    // previous kernel's L2 tail) measured slower on B200 (tools/prof_by_k.py)
     StepEpi se{k};
-    TRY(launch_spmv(ctx, A, P, se, m + 1, (uint32_t)k));
+    TRY(launch_spmv(ctx, A, P, se, m + 1, (uint32_t)k, 0));
     TRY(finish_global<100>(ctx, P, k, k + 1));
-    TRY(launch_cgs2<SW_CGS2_B>(ctx, P, k, k + 1));
+    TRY(launch_cgs2<SW_CGS2_B>(ctx, P, k, k + 1, 0));
     TRY(finish_global<SW_CGS2_B>(ctx, P, k, k + 1));
-    TRY(launch_cgs2<SW_CGS2_C>(ctx, P, k, R1 + 1));
+    TRY(launch_cgs2<SW_CGS2_C>(ctx, P, k, R1 + 1, 0));
     TRY(finish_global<SW_CGS2_C>(ctx, P, k, R1 + 1));
+  }
+  {
+    const size_t esmem = sizeof(double) * ((size_t)m * m + m + MAX_R1);
+    if (esmem > 48 * 1024)
+      CU(cudaFuncSetAttribute(k_end_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
+    ProfScope ps(ctx, PC_OTHER, 0);
+    k_end_cycle<<<1, 256, esmem, ctx->stream>>>(P);
+    ctx->launches++;
+    CU(cudaGetLastError());
   }
   TRY(launch_sweep<SW_XUPDATE>(ctx, P, 0, m, R1, 0, false));
   if (harvest) {
@@ -950,6 +995,7 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) 
     return PGM_EINVAL;
   }
   auto* ctx = new pgm_context();
+  if (const char* e = std::getenv("PGMRES_PDL")) ctx->pdl = e[0] != '0';
   ctx->device = cfg->device;
   ctx->rank = cfg->rank;
   ctx->world = cfg->world;

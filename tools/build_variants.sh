@@ -1,18 +1,15 @@
 #!/bin/bash
-# Build libpgmres variants for tuning studies into tools/variants/<name>/libpgmres.so
+# Build libpgmres variants for tuning studies into paper_1906_04051_b200/_lib/var/<name>/libpgmres.so
+# (in-tree .so files travel to the GPU box); run with tools/run_variants.sh.
+#   tools/build_variants.sh name1 "-DFLAG=1 ..." name2 "-DFLAG=2" ...
 set -e
 cd "$(dirname "$0")/.."
-rm -rf tools/variants
-mkdir -p tools/variants
-build() {
-  name=$1; shift
-  mkdir -p tools/variants/$name
+mkdir -p paper_1906_04051_b200/_lib/var
+while [ $# -gt 0 ]; do
+  name=$1; flags=$2; shift 2
+  mkdir -p paper_1906_04051_b200/_lib/var/$name
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -lineinfo \
-    -Xcompiler -fPIC -shared "$@" -o tools/variants/$name/libpgmres.so \
+    -Xcompiler -fPIC -shared $flags -o paper_1906_04051_b200/_lib/var/$name/libpgmres.so \
     paper_1906_04051_b200/csrc/pgmres.cu -ldl &
-}
-build m3 -DPGM_SPMV_MINB=3
-build m4 -DPGM_SPMV_MINB=4
-build m5 -DPGM_SPMV_MINB=5
-build m4u8 -DPGM_SPMV_MINB=4 -DPGM_SPMV_UNROLL=8
+done
 wait

@@ -1,12 +1,12 @@
 #!/bin/bash
-# Run the bench (kernel breakdown only) against every tools/variants/*/libpgmres.so
+# Bench (kernel breakdown only) every paper_1906_04051_b200/_lib/var/*/libpgmres.so
 cd "$(dirname "$0")/.."
-for d in tools/variants/*/; do
+for d in paper_1906_04051_b200/_lib/var/*/; do
   name=$(basename $d)
-  PGMRES_LIB=$d/libpgmres.so timeout 300 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/var_$name.json 2>/dev/null
+  PGMRES_LIB=$d/libpgmres.so timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e "$@" > gpurun_out/var_$name.json 2>/dev/null
   python -c "
-import json,sys
+import json
 d=json.load(open('gpurun_out/var_$name.json'))
 k=d['kernels']
-print('$name', d['value'], d['ms_per_step'], 'spmv', k['step_spmv']['GBps'], 'B', k['cgs2_pass2_dots']['GBps'], 'C', k['cgs2_update_norm']['GBps'], 'res', k['residual_spmv']['GBps'])"
+print('%-10s %8.1f it/s %7.2f ms  spmv %6.2f  B %6.2f  C %6.2f' % ('$name', d['value'], d['ms_per_step'], k['step_spmv']['ms_total'], k['cgs2_pass2_dots']['ms_total'], k['cgs2_update_norm']['ms_total']))"
 done
