@@ -416,3 +416,32 @@ def test_report_csv_round_trip(torch_cuda, ref):
             assert float(tail) == rep.explicit_residual[int(r)]
             closing += 1
     assert closing == len(rep.explicit_residual)
+
+
+@pytest.mark.slow
+def test_cfg3_deflated_full_size(torch_cuda, golden):
+    """BASELINE config 3 on one B200: n_e = 125 (15,813,251 DOF, 991,266,025 nnz),
+    GMRES(50) + deflation, tol 1e-10, assembled on the device (bit-identical to
+    the reference assembly at u = 0).  The reference run (tests/golden/
+    make_golden_large.py, 8 threads, 24 min) gives 24 restarts / 1181 inner
+    with truncation active from restart 20; histories within 1e-10 * beta0,
+    solution norm and a strided sample within 1e-8."""
+    torch = torch_cuda
+    g = golden("cfg3_defl")
+    ex = pg.DeviceExecutor()
+    A, b = ex.assemble_bratu(125, 6.8, device=True)
+    d = pg.Deflator(pg.DeflationConfig(), ex)
+    x = torch.zeros(ex.n_own, dtype=torch.float64, device="cuda")
+    rep = pg.deflated_gmres(A, b, x, pg.GmresConfig(m=50, rel_tol=1e-10), d, ex)
+    assert rep.converged
+    assert abs(rep.restarts - int(g["restarts"])) <= 1
+    _compare(rep, g, None)
+    xh = x.cpu().numpy()
+    xn = float(g["x_norm"])
+    assert abs(np.linalg.norm(xh) - xn) <= X_TOL * xn
+    s = int(g["stride"])
+    assert np.linalg.norm(xh[::s] - g["x_sample"]) <= X_TOL * np.linalg.norm(g["x_sample"]) * 10
+    assert d.rank() == int(g["rank"])
+    hr = np.array([h.r for h in d.history()])
+    k = min(len(hr), len(g["hist_r"]))
+    assert np.array_equal(hr[:k], g["hist_r"][:k]), (hr, g["hist_r"])
