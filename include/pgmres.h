@@ -14,6 +14,7 @@
  *   pgm_spmv ................. Executor::spmv                       parallel.hpp:93
  *   pgm_deflator_* ........... class Deflator                       deflation.hpp:35-89
  *   pgm_report_* ............. GmresReport / write_csv              gmres.hpp:31-44
+ *   pgm_newton_solve ......... newton_solve (caller of the path)    newton.hpp:45-54
  *
  * Conventions: plain pointers and sizes; every function returns a pgm_status
  * (0 = OK).  The message of the last failure is pgm_last_error(ctx).  Host
@@ -189,6 +190,48 @@ pgm_status pgm_bratu_nnz(const pgm_context* ctx, uint32_t n_e, uint64_t* nnz);
 pgm_status pgm_bratu_assemble(pgm_context* ctx, uint32_t n_e, double lambda, const double* u,
                               int32_t flags, uint32_t* row_ptr, uint32_t* col_idx,
                               double* values, double* rhs);
+
+/* ---- caller side: the Newton driver -------------------------------------- *
+ * newton_solve (newton.hpp:45-54, newton.cpp:31-97) for the Bratu problem on
+ * the (2 n_e + 1)^3 mesh, device-resident: assembly, deflated PGMRES solve,
+ * update and norms run on the GPU; the host reads two scalars per iteration.
+ * u is the GLOBAL iterate (n_global entries; initial guess in, solution out:
+ * every rank writes its owned rows).  Same stopping rule and records as the
+ * reference: stop when ||delta||_inf <= update_tol, optional lambda
+ * continuation.  Errors: EINVAL for max_iters = 0 ("newton: max_iters must be
+ * positive"), plus every pgm_solve error. */
+typedef struct { /* NewtonConfig, newton.hpp:15-23 */
+  uint32_t max_iters;
+  double update_tol;
+  pgm_gmres_config gmres;
+  pgm_deflation_config deflation;
+  int32_t use_deflation;
+  int32_t continuation;
+  uint32_t continuation_steps;
+} pgm_newton_config;
+
+typedef struct { /* NewtonIterRecord, newton.hpp:25-32 */
+  uint32_t iter;
+  double lambda;
+  double update_inf;
+  double residual_norm;
+  uint32_t gmres_restarts;
+  uint64_t gmres_inner;
+} pgm_newton_record;
+
+typedef struct { /* NewtonReport, newton.hpp:34-43 (iters owned; pgm_newton_report_free) */
+  pgm_newton_record* iters;
+  uint32_t n_iters;
+  int32_t converged;
+  double final_residual;
+  double final_update;
+  uint64_t total_inner;
+  double seconds; /* wall time of the driver (host clock) */
+} pgm_newton_report;
+
+pgm_status pgm_newton_solve(pgm_context* ctx, uint32_t n_e, double lambda, double* u,
+                            int32_t flags, const pgm_newton_config* cfg, pgm_newton_report* rep);
+void pgm_newton_report_free(pgm_newton_report* rep);
 
 #ifdef __cplusplus
 }

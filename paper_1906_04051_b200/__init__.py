@@ -6,11 +6,13 @@ solver API over that ABI.
 """
 from .dgmres import (CsrMatrix, DeflationConfig, DeflationRecord, Deflator, DeviceCsr,
                      DeviceError, DeviceExecutor, GmresConfig, GmresError, GmresReport,
-                     InnerRecord, LoopbackGroup, deflated_gmres, gmres_restarted,
-                     nccl_unique_id)
+                     InnerRecord, LoopbackGroup, NewtonConfig, NewtonIterRecord,
+                     NewtonReport, deflated_gmres, gmres_restarted, nccl_unique_id,
+                     newton_solve)
 
 __all__ = [
     "CsrMatrix", "DeflationConfig", "DeflationRecord", "Deflator", "DeviceCsr", "DeviceError",
     "DeviceExecutor", "GmresConfig", "GmresError", "GmresReport", "InnerRecord",
-    "LoopbackGroup", "deflated_gmres", "gmres_restarted", "nccl_unique_id",
+    "LoopbackGroup", "NewtonConfig", "NewtonIterRecord", "NewtonReport", "deflated_gmres",
+    "gmres_restarted", "nccl_unique_id", "newton_solve",
 ]

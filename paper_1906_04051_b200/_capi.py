@@ -52,6 +52,26 @@ class DeflationRecordC(C.Structure):
                 ("smallest_ritz", C.c_double)]
 
 
+class NewtonConfigC(C.Structure):
+    _fields_ = [("max_iters", C.c_uint32), ("update_tol", C.c_double),
+                ("gmres", GmresConfigC), ("deflation", DeflationConfigC),
+                ("use_deflation", C.c_int32), ("continuation", C.c_int32),
+                ("continuation_steps", C.c_uint32)]
+
+
+class NewtonRecordC(C.Structure):
+    _fields_ = [("iter", C.c_uint32), ("lam", C.c_double), ("update_inf", C.c_double),
+                ("residual_norm", C.c_double), ("gmres_restarts", C.c_uint32),
+                ("gmres_inner", C.c_uint64)]
+
+
+class NewtonReportC(C.Structure):
+    _fields_ = [("iters", C.POINTER(NewtonRecordC)), ("n_iters", C.c_uint32),
+                ("converged", C.c_int32), ("final_residual", C.c_double),
+                ("final_update", C.c_double), ("total_inner", C.c_uint64),
+                ("seconds", C.c_double)]
+
+
 # Every symbol the header declares (tests check the .so exports all of them).
 EXPORTS = [
     "pgm_context_create", "pgm_context_destroy", "pgm_last_error", "pgm_context_partition",
@@ -62,7 +82,7 @@ EXPORTS = [
     "pgm_deflator_observe_ritz", "pgm_deflator_apply", "pgm_solve", "pgm_report_free",
     "pgm_context_launch_count", "pgm_context_set_profiling", "pgm_context_profile",
     "pgm_bratu_nnz", "pgm_bratu_assemble", "pgm_nccl_unique_id", "pgm_loopback_create",
-    "pgm_loopback_destroy",
+    "pgm_loopback_destroy", "pgm_newton_solve", "pgm_newton_report_free",
 ]
 
 _lib = None
@@ -114,6 +134,9 @@ def lib():
         "pgm_nccl_unique_id": ([vp], C.c_int),
         "pgm_loopback_create": ([i32, C.POINTER(vp)], C.c_int),
         "pgm_loopback_destroy": ([vp], None),
+        "pgm_newton_solve": ([vp, u32, dbl, vp, i32, C.POINTER(NewtonConfigC),
+                              C.POINTER(NewtonReportC)], C.c_int),
+        "pgm_newton_report_free": ([C.POINTER(NewtonReportC)], None),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -1203,4 +1203,55 @@ __global__ void k_copy(double* __restrict__ out, const double* __restrict__ in, 
     out[i] = in[i];
 }
 
+
+// ---------------------------------------------------------------------------
+// Newton driver scalars (newton.cpp:54,72-73): per-block partials of
+// sum rhs^2 (rhs = -R(u)) and of max|delta| with u += delta fused in; a
+// one-block kernel combines the partials in block order (deterministic).
+__global__ void __launch_bounds__(256) k_newton_partials(const double* __restrict__ rhs,
+                                                         const double* __restrict__ delta,
+                                                         double* __restrict__ u, int n,
+                                                         double* part) {
+  __shared__ double s_sum[8], s_max[8];
+  double sq = 0.0, mx = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (rhs) sq += rhs[i] * rhs[i];
+    if (delta) {
+      const double d = delta[i];
+      u[i] = u[i] + d;  // ex.axpy(1.0, delta, u)
+      mx = fmax(mx, fabs(d));
+    }
+  }
+  sq = warp_sum(sq);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    s_sum[warp] = sq;
+    s_max[warp] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += s_sum[w];
+      b = fmax(b, s_max[w]);
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+__global__ void k_newton_final(const double* part, int G, double* out, int nv, int rank) {
+  if (threadIdx.x != 0) return;
+  double a = 0.0, b = 0.0;
+  for (int q = 0; q < G; ++q) {
+    a += part[2 * q];
+    b = fmax(b, part[2 * q + 1]);
+  }
+  for (int v = 0; v < nv; ++v) out[v] = 0.0;
+  out[0] = a;
+  out[1 + rank] = b;
+}
+
 }  // namespace pgm

@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <mutex>
@@ -133,6 +134,7 @@ struct pgm_context {
   void* nccl = nullptr;
   struct pgm_loopback* loop = nullptr;
   pgm_deflator* cur_defl = nullptr;  // deflator of the running solve (halo of u)
+  double* halo_ptr = nullptr;        // HV_PTR: ctx-layout view of a caller vector (Newton u)
   // optional per-launch profiling (CUDA events around every hot-path kernel)
   bool prof_on = false;
   bool pdl = true;  // programmatic dependent launch of the hot-path kernels (PGMRES_PDL=0 disables)
@@ -562,7 +564,7 @@ Status set_gstate_idle(pgm_context* ctx) {
 // ---------------------------------------------------------------------------
 // Multi-GPU collectives (world > 1): allreduce of the block-reduced sums,
 // then the scalar finisher on every rank.
-enum HaloKind { HV_V = 0, HV_X = 1, HV_U = 2, HV_TMP = 3 };
+enum HaloKind { HV_V = 0, HV_X = 1, HV_U = 2, HV_TMP = 3, HV_PTR = 4 };
 Status allreduce_red(pgm_context* ctx, int nv);
 Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot = 0);
 
@@ -908,6 +910,7 @@ double* halo_vec(pgm_context* ctx, HaloKind kind, int slot) {
     case HV_X: return ctx->x;
     case HV_U: return ctx->cur_defl ? ctx->cur_defl->u : nullptr;
     case HV_TMP: return ctx->tmp;
+    case HV_PTR: return ctx->halo_ptr;
   }
   return nullptr;
 }
@@ -1623,6 +1626,190 @@ pgm_status pgm_bratu_assemble(pgm_context* ctx, uint32_t n_e, double lambda, con
   cudaSetDevice(ctx->device);
   Status s = bratu_assemble(ctx, n_e, lambda, u, flags, row_ptr, col_idx, values, rhs);
   return s.code ? fail(ctx, s) : PGM_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Newton driver (newton.hpp:15-54, newton.cpp:31-97), device-resident: u, the
+// Jacobian (pattern built once, values rewritten in place, assembly.cpp:253),
+// -R(u), delta and the deflation basis stay in HBM; the host reads two
+// scalars per Newton iteration (||R||_2, ||delta||_inf) plus the solve's
+// per-restart status word.
+namespace {
+
+Status newton_scalars(pgm_context* ctx, const double* rhs_own, const double* delta_own,
+                      double* u_own, double* res_norm, double* step) {
+  // red_out[0] = sum rhs^2 (global), red_out[1 + q] = max|delta| of rank q
+  const int nv = 1 + ctx->world;
+  TRY(ensure_reduction(ctx, nv));
+  const int G = ctx->nsm * 4;
+  k_newton_partials<<<G, 256, 0, ctx->stream>>>(rhs_own, delta_own, u_own, (int)ctx->n,
+                                                ctx->part_buf);
+  k_newton_final<<<1, 256, 0, ctx->stream>>>(ctx->part_buf, G, ctx->red_out, nv, ctx->rank);
+  ctx->launches += 2;
+  CU(cudaGetLastError());
+  if (ctx->world > 1) TRY(allreduce_red(ctx, nv));
+  double h[1 + 64];
+  CU(cudaMemcpyAsync(h, ctx->red_out, 8 * (size_t)nv, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (res_norm) *res_norm = std::sqrt(h[0]);
+  if (step) {
+    double m = 0.0;
+    for (int q = 0; q < ctx->world; ++q) m = std::max(m, h[1 + q]);
+    *step = m;
+  }
+  return {};
+}
+
+Status newton_impl(pgm_context* ctx, uint32_t n_e, double lambda, double* u, int32_t flags,
+                   const pgm_newton_config* cfg, pgm_newton_report* rep) {
+  if (!cfg) return einval("newton: null config");
+  if (cfg->max_iters == 0) return einval("newton: max_iters must be positive");
+  if (ctx->world > 64) return einval("newton: world > 64");
+  const uint64_t na = 2ull * n_e + 1;
+  if (n_e == 0 || na * na * na != ctx->n_global)
+    return einval("newton: (2 n_e + 1)^3 != context n_global");
+  const size_t N = ctx->n_global, n = ctx->n;
+  const size_t rb = ctx->part.row_begin;
+  uint64_t nnz = 0;
+  nnz = bratu_rows_nnz(n_e, ctx->part.row_begin, ctx->part.row_end);
+  struct Bufs {
+    double *ug = nullptr, *va = nullptr, *rhs = nullptr, *delta = nullptr;
+    unsigned *rp = nullptr, *ci = nullptr;
+    pgm_matrix* J = nullptr;
+    pgm_deflator* D = nullptr;
+    ~Bufs() {
+      dfree(ug);
+      dfree(va);
+      dfree(rhs);
+      dfree(delta);
+      dfree(rp);
+      dfree(ci);
+      if (J) pgm_matrix_destroy(J);
+      if (D) pgm_deflator_destroy(D);
+    }
+  } B;
+  // u: global iterate (every rank holds the full-size vector; only its
+  // [halo_lo | own | halo_hi] window is kept current, which is all the
+  // assembly of its rows reads)
+  TRY(dalloc(&B.ug, N));
+  TRY(dalloc(&B.va, nnz));
+  TRY(dalloc(&B.rhs, n));
+  TRY(dalloc(&B.delta, n));
+  TRY(dalloc(&B.rp, n + 1));
+  TRY(dalloc(&B.ci, nnz));
+  CU(cudaMemcpyAsync(B.ug, u, 8 * N,
+                     (flags & PGM_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     ctx->stream));
+  double* u_own = B.ug + rb;
+  ctx->halo_ptr = B.ug + rb - ctx->lo;  // ctx layout [halo_lo | own | halo_hi]
+  if (cfg->use_deflation) {
+    const pgm_status st = pgm_deflator_create(ctx, &cfg->deflation, &B.D);
+    if (st != PGM_OK) return Status{st, ctx->err};
+  }
+  std::vector<double> stages;
+  if (cfg->continuation && cfg->continuation_steps > 1) {
+    for (uint32_t q = 1; q <= cfg->continuation_steps; ++q)
+      stages.push_back(lambda * double(q) / double(cfg->continuation_steps));
+  } else {
+    stages.push_back(lambda);
+  }
+  std::vector<pgm_newton_record> recs;
+  const auto t0 = std::chrono::steady_clock::now();
+  uint32_t iter = 0;
+  uint64_t total_inner = 0;
+  double final_residual = 0.0, final_update = 0.0;
+  bool converged = true;
+  for (double lam : stages) {
+    bool stage_done = false;
+    for (uint32_t it = 0; it < cfg->max_iters; ++it) {
+      // assemble_residual + assemble_jacobian (newton.cpp:53-57): rhs = -R(u)
+      TRY(bratu_assemble(ctx, n_e, lam, B.ug, PGM_DEVICE_PTRS, B.rp, B.ci, B.va, B.rhs));
+      double res_norm = 0.0;
+      TRY(newton_scalars(ctx, B.rhs, nullptr, nullptr, &res_norm, nullptr));
+      if (!B.J) {
+        pgm_csr_view v{(uint32_t)n, nnz, B.rp, B.ci, B.va};
+        TRY(matrix_upload(ctx, &v, PGM_DEVICE_PTRS, &B.J));
+      } else {
+        const pgm_status st = pgm_matrix_update_values(B.J, B.va, PGM_DEVICE_PTRS);
+        if (st != PGM_OK) return Status{st, ctx->err};
+      }
+      CU(cudaMemsetAsync(B.delta, 0, 8 * n, ctx->stream));
+      if (B.D) {
+        const pgm_status st = pgm_deflator_reset(B.D);  // newton.cpp:62
+        if (st != PGM_OK) return Status{st, ctx->err};
+      }
+      pgm_report lin{};
+      Status ss = solve_impl(ctx, B.J, B.D, B.rhs, B.delta, &cfg->gmres, PGM_DEVICE_PTRS, &lin);
+      const uint32_t lin_restarts = lin.restarts;
+      const uint64_t lin_inner = lin.total_inner;
+      pgm_report_free(&lin);
+      TRY(ss);
+      // u += delta, ||delta||_inf (newton.cpp:72-73)
+      double step = 0.0;
+      TRY(newton_scalars(ctx, nullptr, B.delta, u_own, nullptr, &step));
+      if (ctx->world > 1) TRY(halo_exchange(ctx, HV_PTR));
+      ++iter;
+      recs.push_back(pgm_newton_record{iter, lam, step, res_norm, lin_restarts, lin_inner});
+      total_inner += lin_inner;
+      final_update = step;
+      final_residual = res_norm;
+      if (step <= cfg->update_tol) {
+        stage_done = true;
+        break;
+      }
+    }
+    if (!stage_done) {
+      converged = false;
+      break;
+    }
+  }
+  if (converged) {
+    TRY(bratu_assemble(ctx, n_e, stages.back(), B.ug, PGM_DEVICE_PTRS, B.rp, B.ci, B.va, B.rhs));
+    TRY(newton_scalars(ctx, B.rhs, nullptr, nullptr, &final_residual, nullptr));
+  }
+  const double secs =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  // u out: every rank writes its owned rows (the caller's global vector)
+  CU(cudaMemcpyAsync(u + rb, u_own, 8 * n,
+                     (flags & PGM_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->halo_ptr = nullptr;
+  if (rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->n_iters = (uint32_t)recs.size();
+    rep->iters = (pgm_newton_record*)std::malloc(sizeof(pgm_newton_record) *
+                                                 std::max<size_t>(1, recs.size()));
+    if (!recs.empty()) std::memcpy(rep->iters, recs.data(), sizeof(pgm_newton_record) * recs.size());
+    rep->converged = converged;
+    rep->final_residual = final_residual;
+    rep->final_update = final_update;
+    rep->total_inner = total_inner;
+    rep->seconds = secs;
+  }
+  return {};
+}
+
+}  // namespace
+
+extern "C" {
+
+pgm_status pgm_newton_solve(pgm_context* ctx, uint32_t n_e, double lambda, double* u,
+                            int32_t flags, const pgm_newton_config* cfg, pgm_newton_report* rep) {
+  if (!ctx || !u) return PGM_EINVAL;
+  cudaSetDevice(ctx->device);
+  Status s = newton_impl(ctx, n_e, lambda, u, flags, cfg, rep);
+  ctx->halo_ptr = nullptr;
+  return s.code ? fail(ctx, s) : PGM_OK;
+}
+
+void pgm_newton_report_free(pgm_newton_report* rep) {
+  if (!rep) return;
+  std::free(rep->iters);
+  rep->iters = nullptr;
+  rep->n_iters = 0;
 }
 
 }  // extern "C"

@@ -570,3 +570,88 @@ def gmres_restarted(opA, opM, b, x, cfg: GmresConfig, ex: DeviceExecutor,
     if not isinstance(opA, (CsrMatrix, DeviceCsr)):
         raise ValueError("gmres_restarted: opA must be a CsrMatrix or DeviceCsr")
     return _solve(opA, b, x, cfg, None, ex)
+
+
+# ---------------------------------------------------------------------------
+# Newton driver (newton.hpp:15-54): the caller of the linear-solve path, run
+# device-resident by pgm_newton_solve.
+
+@dataclass
+class NewtonConfig:
+    """NewtonConfig (newton.hpp:15-23)."""
+    max_iters: int = 30
+    update_tol: float = 1e-8
+    gmres: GmresConfig = field(default_factory=lambda: GmresConfig(m=50, max_restarts=100,
+                                                                   rel_tol=1e-10))
+    deflation: DeflationConfig = field(default_factory=DeflationConfig)
+    use_deflation: bool = True
+    continuation: bool = False
+    continuation_steps: int = 4
+
+    def _c(self):
+        if self.max_iters < 0 or self.continuation_steps < 0:
+            raise ValueError("NewtonConfig: negative size")
+        return capi.NewtonConfigC(int(self.max_iters), float(self.update_tol), self.gmres._c(),
+                                  self.deflation._c(), int(bool(self.use_deflation)),
+                                  int(bool(self.continuation)), int(self.continuation_steps))
+
+
+@dataclass
+class NewtonIterRecord:
+    """NewtonIterRecord (newton.hpp:25-32)."""
+    iter: int
+    lam: float
+    update_inf: float
+    residual_norm: float
+    gmres_restarts: int
+    gmres_inner: int
+
+
+@dataclass
+class NewtonReport:
+    """NewtonReport (newton.hpp:34-43)."""
+    iters: list = field(default_factory=list)
+    converged: bool = False
+    final_residual: float = 0.0
+    final_update: float = 0.0
+    total_inner: int = 0
+    seconds: float = 0.0
+
+    def write_csv(self, os_=None) -> str:
+        """iter,update_inf_norm,residual_2norm,gmres_restarts (newton.cpp:12-19)."""
+        s = "iter,update_inf_norm,residual_2norm,gmres_restarts\n" + "".join(
+            f"{r.iter},{_g17(r.update_inf)},{_g17(r.residual_norm)},{r.gmres_restarts}\n"
+            for r in self.iters)
+        if os_ is not None:
+            os_.write(s)
+        return s
+
+
+def newton_solve(n_e: int, lam: float, u, cfg: NewtonConfig, ex: DeviceExecutor) -> NewtonReport:
+    """newton_solve(build_mesh(n_e), lambda, u, cfg, ex) (newton.hpp:53-54).
+
+    u: global iterate ((2 n_e + 1)^3 float64, numpy or CUDA tensor), initial
+    guess in and solution out (each rank writes its owned rows)."""
+    na = 2 * int(n_e) + 1
+    ex._ensure(na ** 3)
+    if _is_cuda(u):
+        up, fl = u.data_ptr(), capi.PGM_DEVICE_PTRS
+    else:
+        if not (isinstance(u, np.ndarray) and u.dtype == np.float64 and u.flags.c_contiguous):
+            raise ValueError("u must be a contiguous float64 numpy array (updated in place)")
+        up, fl = u.ctypes.data, 0
+    if (u.numel() if _is_cuda(u) else u.size) != na ** 3:
+        raise ValueError("u must hold (2 n_e + 1)^3 entries")
+    c = cfg._c()
+    rep = capi.NewtonReportC()
+    L = capi.lib()
+    _check(L.pgm_newton_solve(ex.handle, int(n_e), float(lam), up, fl, C.byref(c), C.byref(rep)),
+           ex.handle)
+    try:
+        its = [NewtonIterRecord(int(r.iter), float(r.lam), float(r.update_inf),
+                                float(r.residual_norm), int(r.gmres_restarts),
+                                int(r.gmres_inner)) for r in rep.iters[: rep.n_iters]]
+        return NewtonReport(its, bool(rep.converged), rep.final_residual, rep.final_update,
+                            int(rep.total_inner), rep.seconds)
+    finally:
+        L.pgm_newton_report_free(C.byref(rep))
