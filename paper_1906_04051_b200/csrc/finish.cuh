@@ -144,41 +144,41 @@ __device__ __forceinline__ void fin_step_spmv(const Params& P, int k, const doub
   }
 }
 
-// After CGS2 pass 2 dots: red[l] = W_l . w1.  h = h1 + h2 (gmres.cpp:50-53).
-__device__ __forceinline__ void fin_sweep_b(const Params& P, int k, const double* red) {
-  const size_t col = (size_t)k * (P.m + 1);
-  for (int l = threadIdx.x; l <= k; l += blockDim.x) {
-    const double h2 = P.s[l] * red[l];
-    P.coefB[l] = -h2 * P.s[l];
-    const double h = P.h1[l] + h2;
-    P.h_orig[col + l] = h;
-    P.h_rot[col + l] = h;
-  }
-}
-
-// After CGS2 pass 2 update: red[0] = ||w2||^2, red[1+l] = U_l . w2.
-// h_{k+1,k}, Givens update, records and the inner-loop exits
-// (gmres.cpp:58-90, 163-180).
-__device__ void fin_sweep_c(const Params& P, int k, const double* red) {
-  __shared__ double sH[MAX_M + 2], sC[MAX_M], sS[MAX_M];
+// After CGS2 pass 2 (update w1 and its dots), gmres.cpp:50-65 + 67-90:
+//   red[l] = W_l . w1 (l <= k), red[k+1] = ||w1||^2, red[k+2+j] = U_j . w1.
+// h = h1 + h2; pass C (w2 = w1 - V h2, k_cgs2_update) needs no reduction:
+//   ||w2||^2 = ||w1||^2 - ||h2||^2                 (V orthonormal)
+//   U^T W_{k+1} = U^T w1 - sum_l h2_l U^T v_l      (U^T v_l kept in tU)
+// then h_{k+1,k}, the Givens update, the records and the inner-loop exits
+// (gmres.cpp:163-180), and the deflation coefficients of the next apply.
+__device__ void fin_sweep_b(const Params& P, int k, const double* red) {
+  __shared__ double sH[MAX_M + 2], sC[MAX_M], sS[MAX_M], sh2[MAX_M + 1];
   __shared__ int s_go;
   GState* g = P.g;
   const int m = P.m;
   const size_t col = (size_t)k * (m + 1);
-  for (int i = threadIdx.x; i <= k; i += blockDim.x) {
-    sH[i] = P.h_rot[col + i];
-    if (i < k) {
-      sC[i] = P.cs[i];
-      sS[i] = P.sn[i];
+  for (int l = threadIdx.x; l <= k; l += blockDim.x) {
+    const double sl = P.s[l];
+    const double h2 = sl * red[l];
+    sh2[l] = h2;
+    P.coefB[l] = -h2 * sl;
+    const double h = P.h1[l] + h2;
+    P.h_orig[col + l] = h;
+    sH[l] = h;
+    if (l < k) {
+      sC[l] = P.cs[l];
+      sS[l] = P.sn[l];
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     s_go = 0;
-    const double hnext = sqrt(red[0]);
+    double nh2 = 0.0;
+    for (int l = 0; l <= k; ++l) nh2 += sh2[l] * sh2[l];
+    const double hnext = sqrt(fmax(red[k + 1] - nh2, 0.0));
     sH[k + 1] = hnext;
     P.h_orig[col + k + 1] = hnext;
-    if (!isfinite(hnext)) {
+    if (!isfinite(hnext) || !isfinite(red[k + 1])) {
       set_error(P, 2, g->restart, k);
     } else {
       P.s[k + 1] = hnext > 0.0 ? 1.0 / hnext : 0.0;
@@ -226,10 +226,14 @@ __device__ void fin_sweep_c(const Params& P, int k, const double* red) {
   __syncthreads();
   for (int i = threadIdx.x; i <= k + 1; i += blockDim.x) P.h_rot[col + i] = sH[i];
   if (s_go) {
-    const int r = P.d->r;
-    double* t = P.tU + (size_t)(k + 1) * P.R1;
+    const int r = P.d->r, R1 = P.R1;
+    double* t = P.tU + (size_t)(k + 1) * R1;
     const double sk1 = P.s[k + 1];
-    for (int l = threadIdx.x; l < r; l += blockDim.x) t[l] = red[1 + l] * sk1;
+    for (int j = threadIdx.x; j < r; j += blockDim.x) {
+      double uw = red[k + 2 + j];
+      for (int l = 0; l <= k; ++l) uw -= sh2[l] * P.tU[(size_t)l * R1 + j];
+      t[j] = uw * sk1;
+    }
     __syncthreads();
     defl_coeffs_par(P, r, t, P.c);
   }

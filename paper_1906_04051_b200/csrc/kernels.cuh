@@ -416,6 +416,7 @@ struct SweepSpec {
   int nq;
   int qstaged;
   int selfnorm;
+  int normlast;  // the self-norm is value nq (after the dots), not value 0
   int skip;
 };
 
@@ -426,6 +427,7 @@ __device__ __forceinline__ SweepSpec sweep_spec(const Params& P, int k) {
   const DState* d = P.d;
   const size_t lo = P.lo;
   if (MODE == SW_CGS2_B) {
+    // generic path (np > 112, plain GMRES only: r = 0): W_l . w1 then ||w1||^2
     S.skip = !g->active;
     S.in = S.out = P.V + (size_t)(k + 1) * P.ld + lo;
     S.Pv = P.V + lo;
@@ -434,6 +436,8 @@ __device__ __forceinline__ SweepSpec sweep_spec(const Params& P, int k) {
     S.Q = S.Pv;
     S.nq = k + 1;
     S.qstaged = 1;
+    S.selfnorm = 1;
+    S.normlast = 1;
   } else if (MODE == SW_CGS2_C) {
     S.skip = !g->active;
     S.in = S.out = P.V + (size_t)(k + 1) * P.ld + lo;
@@ -501,7 +505,6 @@ template <int MODE>
 __device__ __forceinline__ void sweep_finish(const Params& P, int k, const double* red) {
   // block-collective (finish.cuh); the push_vector scalars run on thread 0
   if (MODE == SW_CGS2_B) fin_sweep_b(P, k, red);
-  if (MODE == SW_CGS2_C) fin_sweep_c(P, k, red);
   if (MODE == SW_PUSH1 && threadIdx.x == 0) fin_push1(P, red);
   if (MODE == SW_PUSH2 && threadIdx.x == 0) fin_push2(P, red);
   if (MODE == SW_PUSH3 && threadIdx.x == 0) fin_push3(P, red);
@@ -533,7 +536,7 @@ __global__ void __launch_bounds__(SW_BLOCK) k_sweep(Params P, int k) {
   const SweepSpec S = sweep_spec<MODE>(P, k);
   if (S.skip) return;
   const int nv = S.nq + S.selfnorm;
-  const int so = S.selfnorm;
+  const int so = S.selfnorm && !S.normlast;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* tp = sm + warp * TP_DOUBLES;
   double* wacc = sm + SW_WARPS * TP_DOUBLES;
@@ -610,8 +613,8 @@ __global__ void __launch_bounds__(SW_BLOCK) k_sweep(Params P, int k) {
     if (ok) S.out[row] = o;
     else o = 0.0;
     if (nv == 0) continue;
-    if (S.qstaged && NP > 0) {
-      // products with the register-resident P set (no selfnorm in staged modes)
+    if (S.qstaged && NP > 0 && !S.selfnorm) {
+      // products with the register-resident P set
 #pragma unroll
       for (int sl = 0; sl < (NP + TPR - 1) / TPR; ++sl) {
         if (sl * TPR >= nv) continue;
@@ -628,6 +631,7 @@ __global__ void __launch_bounds__(SW_BLOCK) k_sweep(Params P, int k) {
       const double* q = (S.qstaged ? S.Pv : S.Q) + row;
       tp_all(tp, acc, nv, lane, [&](int vv) {
         if (!ok) return 0.0;
+        if (S.normlast) return vv == S.nq ? o * o : __ldg(q + (size_t)vv * ld) * o;
         return (so && vv == 0) ? o * o : __ldg(q + (size_t)(vv - so) * ld) * o;
       });
     }
@@ -666,9 +670,9 @@ __device__ __forceinline__ void store_rows(double* p, const double (&o)[RPL]) {
   }
 }
 
-// CGS2 sweeps, vector set split across the warps of a block (tools/sweepbench.cu).
-//   SW_CGS2_B: w1 = w + sum_l a_l W_l ; dots W_l . w1
-//   SW_CGS2_C: w2 = w1 + sum_l b_l W_l ; ||w2||^2 and U_j . w2
+// CGS2 pass B, vector set split across the warps of a block (tools/sweepbench.cu):
+//   w1 = w + sum_l a_l W_l ; dots W_l . w1, ||w1||^2 and U_j . w1
+// (pass C is then a reduction-free update, k_cgs2_update).
 // All NW warps of a block work on the same chunk of 32*RPL rows (lane = RPL
 // consecutive rows).  Warp q streams the basis vectors l = q + NW*j (j < NPW)
 // and, in pass C, the deflation vectors U_j, j = q + NW*i, so every warp keeps
@@ -683,16 +687,16 @@ __device__ __forceinline__ void store_rows(double* p, const double (&o)[RPL]) {
 // rev: walk the chunks from the end of the vectors.  Consecutive hot-path
 // kernels alternate direction, so each one starts on the rows whose basis
 // entries the previous kernel left in the 126 MB L2.
-template <int MODE, int NW, int RPL, int NPW>
+// NUW: deflation vectors per warp (covers the rank r of this cycle; the host
+// picks the instantiation), NPW: basis vectors per warp.
+template <int MODE, int NW, int RPL, int NUW, int NPW>
 __global__ void __launch_bounds__(NW * 32) k_cgs2(Params P, int k, int rev) {
-  static_assert(MODE == SW_CGS2_B || MODE == SW_CGS2_C, "CGS2 sweeps only");
-  constexpr bool PC = MODE == SW_CGS2_C;
-  constexpr int NUW = PC ? (MAX_R1 + NW - 1) / NW : 0;
-  constexpr int NA = PC ? NUW + 1 : NPW;
+  static_assert(MODE == SW_CGS2_B, "pass C is k_cgs2_update");
+  constexpr int NA = NPW + NUW + 1;
   constexpr int CR = 32 * RPL;  // rows per chunk
   __shared__ __align__(16) double xs[2][NW][CR];
-  __shared__ double bv[NW * (NA > NPW ? NA : NPW) + 2];
-  __shared__ double redv[NW * (NA > NPW ? NA : NPW) + 2];
+  __shared__ double bv[NW * NA + 2];
+  __shared__ double redv[NW * NA + 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int np = k + 1;
   const int n = P.n;
@@ -710,10 +714,10 @@ __global__ void __launch_bounds__(NW * 32) k_cgs2(Params P, int k, int rev) {
   }
   pdl_wait();
   if (!P.g->active) return;
-  const int r = PC ? P.d->r : 0;
+  const int r = P.d->r;
   double* w = P.V + (size_t)(k + 1) * ld + P.lo;
   const double* U0 = P.U + P.lo;
-  const double* coef = PC ? P.coefB : P.coefA;
+  const double* coef = P.coefA;
   double aw[NPW];
 #pragma unroll
   for (int j = 0; j < NPW; ++j) {
@@ -788,36 +792,31 @@ __global__ void __launch_bounds__(NW * 32) k_cgs2(Params P, int k, int rev) {
           if (row0 + e < n) w[row0 + e] = o[e];
       }
     }
-    if (!PC) {
 #pragma unroll
-      for (int j = 0; j < NPW; ++j)
+    for (int e = 0; e < RPL; ++e) {
 #pragma unroll
-        for (int e = 0; e < RPL; ++e) acc[j] += v[j][e] * o[e];
-    } else {
+      for (int j = 0; j < NPW; ++j) acc[j] += v[j][e] * o[e];
 #pragma unroll
-      for (int e = 0; e < RPL; ++e) {
-        if (warp == 0) acc[NUW] += o[e] * o[e];
-#pragma unroll
-        for (int j = 0; j < NUW; ++j) acc[j] += u[j][e] * o[e];
-      }
+      for (int j = 0; j < NUW; ++j) acc[NPW + j] += u[j][e] * o[e];
+      if (warp == 0) acc[NPW + NUW] += o[e] * o[e];
     }
     buf ^= 1;
   }
   pdl_trigger();
-  // block values: B -> bv[l] = W_l . w1 (l < np); C -> bv[0] = ||w2||^2, bv[1 + j] = U_j . w2
-  const int nv = PC ? 1 + r : np;
+  // block values: bv[l] = W_l . w1 (l < np), bv[np] = ||w1||^2, bv[np + 1 + j] = U_j . w1
+  const int nv = np + 1 + r;
 #pragma unroll
   for (int j = 0; j < NA; ++j) {
-    const double s = warp_sum(acc[j]);
+    const double sum = warp_sum(acc[j]);
     if (lane == 0) {
-      if (!PC) {
+      if (j < NPW) {
         const int l = warp + NW * j;
-        if (l < np) bv[l] = s;
-      } else if (j == NUW) {
-        if (warp == 0) bv[0] = s;
-      } else {
-        const int lu = warp + NW * j;
-        if (lu < r) bv[1 + lu] = s;
+        if (l < np) bv[l] = sum;
+      } else if (j < NPW + NUW) {
+        const int lu = warp + NW * (j - NPW);
+        if (lu < r) bv[np + 1 + lu] = sum;
+      } else if (warp == 0) {
+        bv[np] = sum;
       }
     }
   }
@@ -828,6 +827,55 @@ __global__ void __launch_bounds__(NW * 32) k_cgs2(Params P, int k, int rev) {
     return;
   }
   if (grid_reduce(bv, nv, P, redv)) sweep_finish<MODE>(P, k, redv);
+}
+
+// CGS2 pass C: W_{k+1} = w1 + sum_l b_l W_l (b_l = -h2_l s_l).  No reduction:
+// ||w2||^2 and U^T w2 were formed from pass B's dots (fin_sweep_b), so this is
+// a pure stream: each warp owns 64-row chunks (2 rows per lane), the basis is
+// read in batches of 8 vectors with all loads of a batch in flight.
+constexpr int UPD_BLOCK = 256;
+__global__ void __launch_bounds__(UPD_BLOCK) k_cgs2_update(Params P, int k) {
+  __shared__ double as[MAX_M + 8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int np = k + 1;
+  const int n = P.n;
+  const size_t ld = P.ld;
+  const int nch = (n + 63) >> 6;
+  const int W = gridDim.x * (UPD_BLOCK / 32);
+  const double* V0 = P.V + P.lo;
+  {
+    // ahead of the PDL wait: this warp's first chunk of W_0..W_k into L2
+    const int c = blockIdx.x * (UPD_BLOCK / 32) + warp;
+    if (c < nch)
+      for (int l = lane; l < np; l += 32) tma_prefetch_l2(V0 + (size_t)l * ld + (size_t)c * 64, 512);
+  }
+  pdl_wait();
+  if (!P.g->active) return;
+  for (int l = threadIdx.x; l < np + 8; l += UPD_BLOCK) as[l] = l < np ? P.coefB[l] : 0.0;
+  __syncthreads();
+  double* w = P.V + (size_t)(k + 1) * ld + P.lo;
+  for (int c = blockIdx.x * (UPD_BLOCK / 32) + warp; c < nch; c += W) {
+    const int row0 = c * 64 + 2 * lane;
+    double2 o = *reinterpret_cast<const double2*>(w + row0);
+    for (int l0 = 0; l0 < np; l0 += 8) {
+      double2 t[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        t[j] = (l0 + j < np) ? __ldg(reinterpret_cast<const double2*>(V0 + (size_t)(l0 + j) * ld + row0))
+                             : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        o.x += as[l0 + j] * t[j].x;
+        o.y += as[l0 + j] * t[j].y;
+      }
+    }
+    if (row0 + 1 < n) {
+      *reinterpret_cast<double2*>(w + row0) = o;
+    } else if (row0 < n) {
+      w[row0] = o.x;
+    }
+  }
+  pdl_trigger();
 }
 
 // Cross-GPU path: finisher after the allreduce of P.red_out.

@@ -128,6 +128,7 @@ struct pgm_context {
   int ws_R1 = 0;
   GState* g = nullptr;
   GState* h_status = nullptr;  // pinned
+  DState* h_dstate = nullptr;  // pinned copy of the running deflator's state (rank r)
   pgm_deflator* dummy = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // multi-GPU: NCCL (one process per GPU) or an in-process loopback group
@@ -321,24 +322,25 @@ Status launch_sweep_np(pgm_context* ctx, const Params& P, int k, int nv, int np)
 
 // CGS2 sweeps (np = k + 1): warp-split kernels; 4 warps per block (8 above
 // 64 vectors), 2 rows per lane (tools/sweepbench.cu, tools/run_variants.sh).
-template <int MODE, int NW, int RPL, int NPW>
+template <int MODE, int NW, int RPL, int NUW, int NPW>
 Status launch_cgs2_cfg(pgm_context* ctx, const Params& P, int k, int rev) {
   static int occ = 0;  // per instantiation; same device geometry for every context
-  if (occ == 0) occ = std::min(MAX_SPLIT_BLOCKS_PER_SM, occupancy(k_cgs2<MODE, NW, RPL, NPW>, NW * 32, 0));
+  if (occ == 0)
+    occ = std::min(MAX_SPLIT_BLOCKS_PER_SM, occupancy(k_cgs2<MODE, NW, RPL, NUW, NPW>, NW * 32, 0));
   const int nchunks = (int)((ctx->n + 32 * RPL - 1) / (32 * RPL));
   const int G = std::max(1, std::min(nchunks, occ * ctx->nsm));
   ProfScope ps(ctx, prof_class_sweep<MODE>(), (uint32_t)k);
-  CU(launch_pdl(ctx, k_cgs2<MODE, NW, RPL, NPW>, G, NW * 32, 0, P, k, rev));
+  CU(launch_pdl(ctx, k_cgs2<MODE, NW, RPL, NUW, NPW>, G, NW * 32, 0, P, k, rev));
   ctx->launches++;
   CU(cudaGetLastError());
   return {};
 }
 
-template <int MODE, int NW, int RPL, int... Is>
+template <int MODE, int NW, int RPL, int NUW, int... Is>
 Status launch_cgs2_table(pgm_context* ctx, const Params& P, int k, int rev, int npw,
                          std::integer_sequence<int, Is...>) {
   using Fn = Status (*)(pgm_context*, const Params&, int, int);
-  static constexpr Fn table[] = {&launch_cgs2_cfg<MODE, NW, RPL, Is + 1>...};
+  static constexpr Fn table[] = {&launch_cgs2_cfg<MODE, NW, RPL, NUW, Is + 1>...};
   return table[npw - 1](ctx, P, k, rev);
 }
 
@@ -347,18 +349,44 @@ constexpr int CGS2_SPLIT_MAX = 112;  // = MAX_M: 8 warps x 14 vectors
 #ifndef PGM_CGS2_RPL
 #define PGM_CGS2_RPL 2  // rows per lane (tools/run_variants.sh study: 2 beats 1)
 #endif
-template <int MODE>
-Status launch_cgs2(pgm_context* ctx, const Params& P, int k, int nv, int rev) {
+Status launch_cgs2_update(pgm_context* ctx, const Params& P, int k) {
+  static int occ = 0;
+  if (occ == 0) occ = std::min(MAX_BLOCKS_PER_SM, occupancy(k_cgs2_update, UPD_BLOCK, 0));
+  const int nchunks = (int)((ctx->n + 63) / 64);
+  const int G = std::max(1, std::min((nchunks + UPD_BLOCK / 32 - 1) / (UPD_BLOCK / 32),
+                                     occ * ctx->nsm));
+  ProfScope ps(ctx, PC_SWEEP_C, (uint32_t)k);
+  CU(launch_pdl(ctx, k_cgs2_update, G, UPD_BLOCK, 0, P, k));
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return {};
+}
+
+// NUW (deflation vectors per warp) is chosen from the deflator's current rank
+// r (constant within a cycle; read with the restart status word), so early
+// cycles with a small basis do not pay registers for U.
+template <int NW, int R, int NUW, int NPWMAX>
+Status launch_cgs2_nuw(pgm_context* ctx, const Params& P, int k, int rev, int npw) {
+  return launch_cgs2_table<SW_CGS2_B, NW, R, NUW>(ctx, P, k, rev, npw,
+                                                  std::make_integer_sequence<int, NPWMAX>{});
+}
+
+template <int NW, int R, int NPWMAX>
+Status launch_cgs2_r(pgm_context* ctx, const Params& P, int k, int rev, int npw, int r) {
+  const int nuw = (r + NW - 1) / NW;
+  if (nuw == 0) return launch_cgs2_nuw<NW, R, 0, NPWMAX>(ctx, P, k, rev, npw);
+  if (nuw <= 1) return launch_cgs2_nuw<NW, R, 1, NPWMAX>(ctx, P, k, rev, npw);
+  if (nuw <= 2) return launch_cgs2_nuw<NW, R, 2, NPWMAX>(ctx, P, k, rev, npw);
+  if (nuw <= 4) return launch_cgs2_nuw<NW, R, 4, NPWMAX>(ctx, P, k, rev, npw);
+  return launch_cgs2_nuw<NW, R, (MAX_R1 + NW - 1) / NW, NPWMAX>(ctx, P, k, rev, npw);
+}
+
+Status launch_cgs2_b(pgm_context* ctx, const Params& P, int k, int nv, int rev, int r) {
   constexpr int R = PGM_CGS2_RPL;
   const int np = k + 1;
-  if (MODE == SW_CGS2_B && np <= 4) return launch_cgs2_cfg<MODE, 2, R, 2>(ctx, P, k, rev);
-  if (np <= 64)
-    return launch_cgs2_table<MODE, 4, R>(ctx, P, k, rev, (np + 3) / 4,
-                                         std::make_integer_sequence<int, 16>{});
-  if (np <= CGS2_SPLIT_MAX)
-    return launch_cgs2_table<MODE, 8, R>(ctx, P, k, rev, (np + 7) / 8,
-                                         std::make_integer_sequence<int, 14>{});
-  return launch_sweep_np<MODE, 0>(ctx, P, k, nv, np);
+  if (np <= 64) return launch_cgs2_r<4, R, 16>(ctx, P, k, rev, (np + 3) / 4, r);
+  if (np <= CGS2_SPLIT_MAX) return launch_cgs2_r<8, R, 14>(ctx, P, k, rev, (np + 7) / 8, r);
+  return launch_sweep_np<SW_CGS2_B, 0>(ctx, P, k, nv, np);
 }
 
 // np / nv: upper bounds of the register-streamed set and of the reduced values;
@@ -592,10 +620,9 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
     StepEpi se{k};
     TRY(launch_spmv(ctx, A, P, se, m + 1, (uint32_t)k, 0));
     TRY(finish_global<100>(ctx, P, k, k + 1));
-    TRY(launch_cgs2<SW_CGS2_B>(ctx, P, k, k + 1, 0));
-    TRY(finish_global<SW_CGS2_B>(ctx, P, k, k + 1));
-    TRY(launch_cgs2<SW_CGS2_C>(ctx, P, k, R1 + 1, 0));
-    TRY(finish_global<SW_CGS2_C>(ctx, P, k, R1 + 1));
+    TRY(launch_cgs2_b(ctx, P, k, k + 2 + R1, 0, ctx->cur_defl ? ctx->h_dstate->r : R1));
+    TRY(finish_global<SW_CGS2_B>(ctx, P, k, k + 2 + R1));
+    TRY(launch_cgs2_update(ctx, P, k));
   }
   {
     const size_t esmem = sizeof(double) * ((size_t)m * m + m + MAX_R1);
@@ -640,6 +667,9 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
 }
 
 Status read_status(pgm_context* ctx) {
+  if (ctx->cur_defl)
+    CU(cudaMemcpyAsync(ctx->h_dstate, ctx->cur_defl->d, sizeof(DState), cudaMemcpyDeviceToHost,
+                       ctx->stream));
   CU(cudaMemcpyAsync(ctx->h_status, ctx->g, sizeof(GState), cudaMemcpyDeviceToHost,
                      ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
@@ -1047,6 +1077,9 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) 
   cudaEventCreate(&ctx->ev1);
   Status s;
   if ((s = dalloc(&ctx->g, 1)).code) return bail(s);
+  if ((e = cudaMallocHost(&ctx->h_dstate, sizeof(DState))) != cudaSuccess)
+    return bail(Status{PGM_ENOMEM, "cudaMallocHost"});
+  std::memset(ctx->h_dstate, 0, sizeof(DState));
   if ((e = cudaMallocHost(&ctx->h_status, sizeof(GState))) != cudaSuccess)
     return bail(Status{PGM_ENOMEM, "pinned status"});
   std::memset(ctx->h_status, 0, sizeof(GState));
@@ -1100,6 +1133,7 @@ void pgm_context_destroy(pgm_context* ctx) {
   dfree(ctx->cnt);
   dfree(ctx->red_out);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
+  if (ctx->h_dstate) cudaFreeHost(ctx->h_dstate);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->nccl) nccl_lite::comm_destroy(ctx->nccl);
