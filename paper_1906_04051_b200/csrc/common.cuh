@@ -139,15 +139,19 @@ __device__ __forceinline__ double warp_sum(double v) {
 #define PGM_VPW 4
 #endif
 constexpr int VPW = PGM_VPW;
-__device__ __forceinline__ bool grid_reduce(const double* bvals, int nv, const Params& P,
-                                            double* red) {
+// G / bid: the reduction's block count and this block's index in it (a
+// reduction may span several launches, e.g. the interior and boundary tiles
+// of a halo-overlapped SpMV; partials are indexed by tile, so the order is
+// the same however the launches interleave).
+__device__ __forceinline__ bool grid_reduce_ex(const double* bvals, int nv, const Params& P,
+                                               double* red, int G, int bid) {
   __shared__ int s_flag;
-  const int G = gridDim.x, NG = (G + GROUP - 1) / GROUP;
+  const int NG = (G + GROUP - 1) / GROUP;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int v = threadIdx.x; v < nv; v += blockDim.x) P.part[(size_t)v * G + blockIdx.x] = bvals[v];
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) P.part[(size_t)v * G + bid] = bvals[v];
   __threadfence();
   __syncthreads();
-  const int grp = blockIdx.x / GROUP;
+  const int grp = bid / GROUP;
   const int g0 = grp * GROUP;
   const int gsize = min(GROUP, G - g0);
   if (threadIdx.x == 0) {
@@ -209,6 +213,11 @@ __device__ __forceinline__ bool grid_reduce(const double* bvals, int nv, const P
   if (threadIdx.x == 0) P.cnt[0] = 0;
   __syncthreads();
   return true;
+}
+
+__device__ __forceinline__ bool grid_reduce(const double* bvals, int nv, const Params& P,
+                                            double* red) {
+  return grid_reduce_ex(bvals, nv, P, red, (int)gridDim.x, (int)blockIdx.x);
 }
 
 // Block-wide sum (fixed order), result broadcast to every thread.

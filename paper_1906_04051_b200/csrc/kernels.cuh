@@ -326,14 +326,20 @@ __host__ __device__ constexpr size_t spmv_smem_doubles(int nv) {
 // One 512-row tile per block: SELL SpMV into smem, then every warp runs the
 // epilogue on its 64 rows (2 x 32-row chunks), then the grid reduction.
 // dynamic smem: [small | ys TILE | tp per warp | wacc | bvals nv | red nv]
-template <class Epi>
-__global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params P, Epi E) {
+// Tile segments of one launch of a halo-overlapped SpMV (world > 1): block b
+// runs tile b0 + b for b < len0, else tile b1 + (b - len0); the reduction
+// spans all ntiles tiles of the interior and boundary launches.
+struct SpmvSeg {
+  int b0, len0, b1;
+};
+
+template <class Epi, bool SEG>
+__global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params P, Epi E,
+                                                                 SpmvSeg sg) {
   extern __shared__ double sm[];
-#if PGM_SPMV_REV
-  const int tile = A.rev ? A.ntiles - 1 - (int)blockIdx.x : (int)blockIdx.x;
-#else
-  const int tile = (int)blockIdx.x;
-#endif
+  const int tile = SEG ? ((int)blockIdx.x < sg.len0 ? sg.b0 + (int)blockIdx.x
+                                                    : sg.b1 + ((int)blockIdx.x - sg.len0))
+                       : (int)blockIdx.x;
 #if PGM_SPMV_PREFETCH && PGM_SPMV_EARLY_PF
   {
     // L2 prefetch of this warp's first slice (values + column ids).  The
@@ -382,12 +388,13 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
   pdl_trigger();
   if (nv == 0) return;
   warps_to_block(acc, nv, wacc, bvals);
+  const int G = SEG ? A.ntiles : (int)gridDim.x;
   if (P.world > 1) {
-    if (grid_reduce(bvals, nv, P, red))
+    if (grid_reduce_ex(bvals, nv, P, red, G, tile))
       for (int v = threadIdx.x; v < nv; v += blockDim.x) P.red_out[v] = red[v];
     return;
   }
-  if (grid_reduce(bvals, nv, P, red)) E.finish(P, red);
+  if (grid_reduce_ex(bvals, nv, P, red, G, tile)) E.finish(P, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -1219,6 +1226,18 @@ __global__ void k_observe(DState* d, double v) {
 
 // ---------------------------------------------------------------------------
 // CSR -> SELL conversion: one warp per slice.
+// Rows that read halo columns (global column < rb or >= re; columns ascending
+// per row): out[0] = last such row below, out[1] = first such row above.
+__global__ void k_halo_rows(const unsigned* rp, const unsigned* col, int n, unsigned rb,
+                            unsigned re, int* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned a = rp[i], b = rp[i + 1];
+    if (a == b) continue;
+    if (col[a] < rb) atomicMax(&out[0], i);
+    if (col[b - 1] >= re) atomicMin(&out[1], i);
+  }
+}
+
 __global__ void k_csr_to_sell(Sell A, double* val, unsigned* col, const unsigned* rp,
                               const unsigned* ci, const double* v, unsigned col_shift,
                               int nslices, int write_cols) {

@@ -131,6 +131,9 @@ struct pgm_context {
   DState* h_dstate = nullptr;  // pinned copy of the running deflator's state (rank r)
   pgm_deflator* dummy = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // world > 1: halo planes move on hstream while the interior SpMV tiles run
+  cudaStream_t hstream = nullptr;
+  cudaEvent_t ev_halo_src = nullptr, ev_halo_done = nullptr;
   // multi-GPU: NCCL (one process per GPU) or an in-process loopback group
   void* nccl = nullptr;
   struct pgm_loopback* loop = nullptr;
@@ -162,6 +165,9 @@ struct pgm_matrix {
   unsigned* rp = nullptr;      // device CSR row_ptr (kept for value updates)
   double* vstage = nullptr;    // device CSR values staging
   unsigned col_shift = 0;
+  // tiles [0, t_lo_end) and [t_hi_begin, ntiles) read halo rows; the rest is
+  // interior (world > 1: runs while the halo planes are in flight)
+  int t_lo_end = 0, t_hi_begin = 0;
   Sell view() const {
     Sell S;
     S.sptr = sptr;
@@ -290,18 +296,34 @@ uint32_t prof_class_sweep() {
 
 size_t spmv_smem(int nv) { return sizeof(double) * spmv_smem_doubles(nv); }
 
+// seg: 0 = every tile; 1 = interior tiles; 2 = halo-reading boundary tiles
+// (1 and 2 together form one reduction over all tiles, world > 1).
 template <class Epi>
 Status launch_spmv(pgm_context* ctx, const pgm_matrix* A, const Params& P, const Epi& E,
-                   int nvmax, uint32_t prof_k = 0, int rev = 0) {
+                   int nvmax, uint32_t prof_k = 0, int seg = 0) {
   const size_t smem = spmv_smem(nvmax);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_spmv<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  // one tile per block: the hardware scheduler balances the tiles
-  const int G = std::max(1, A->ntiles);
-  ProfScope ps(ctx, prof_class_of<Epi>(), prof_k);
   Sell sv = A->view();
-  sv.rev = rev;
-  CU(launch_pdl(ctx, k_spmv<Epi>, G, SPMV_THREADS, smem, sv, P, E));
+  SpmvSeg sg{0, 0, 0};
+  int G = std::max(1, A->ntiles);
+  if (seg == 1) {
+    sg = SpmvSeg{A->t_lo_end, A->t_hi_begin - A->t_lo_end, 0};
+    G = sg.len0;
+  } else if (seg == 2) {
+    sg = SpmvSeg{0, A->t_lo_end, A->t_hi_begin};
+    G = A->t_lo_end + (A->ntiles - A->t_hi_begin);
+  }
+  if (G <= 0) return {};
+  ProfScope ps(ctx, prof_class_of<Epi>(), prof_k);
+  // one tile per block: the hardware scheduler balances the tiles
+  if (seg == 0) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_spmv<Epi, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    CU(launch_pdl(ctx, k_spmv<Epi, false>, G, SPMV_THREADS, smem, sv, P, E, sg));
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_spmv<Epi, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    CU(launch_pdl(ctx, k_spmv<Epi, true>, G, SPMV_THREADS, smem, sv, P, E, sg));
+  }
   ctx->launches++;
   CU(cudaGetLastError());
   return {};
@@ -594,7 +616,7 @@ Status set_gstate_idle(pgm_context* ctx) {
 // then the scalar finisher on every rank.
 enum HaloKind { HV_V = 0, HV_X = 1, HV_U = 2, HV_TMP = 3, HV_PTR = 4 };
 Status allreduce_red(pgm_context* ctx, int nv);
-Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot = 0);
+Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot = 0, cudaStream_t st = nullptr);
 
 template <int KIND>
 Status finish_global(pgm_context* ctx, const Params& P, int k, int nv) {
@@ -613,12 +635,32 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
                      bool harvest) {
   const int m = ctx->ws_m;
   const int R1 = d->R1;
+  const bool overlap = ctx->world > 1 && A->t_hi_begin > A->t_lo_end;
   for (int k = 0; k < m; ++k) {
+    if (overlap) {
+      // halo planes of W_k on hstream (NVLink P2P through NCCL send/recv)
+      // while the interior tiles run; then the boundary tiles.  NCCL calls
+      // stay totally ordered: the halo completes before the next allreduce
+      // is enqueued behind the boundary tiles.
+      CU(cudaEventRecord(ctx->ev_halo_src, ctx->stream));
+      CU(cudaStreamWaitEvent(ctx->hstream, ctx->ev_halo_src, 0));
+      TRY(halo_exchange(ctx, HV_V, k, ctx->hstream));
+      CU(cudaEventRecord(ctx->ev_halo_done, ctx->hstream));
+      StepEpi se{k};
+      TRY(launch_spmv(ctx, A, P, se, m + 1, (uint32_t)k, 1));
+      CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo_done, 0));
+      TRY(launch_spmv(ctx, A, P, se, m + 1, (uint32_t)k, 2));
+      TRY(finish_global<100>(ctx, P, k, k + 1));
+      TRY(launch_cgs2_b(ctx, P, k, k + 2 + R1, 0, ctx->cur_defl ? ctx->h_dstate->r : R1));
+      TRY(finish_global<SW_CGS2_B>(ctx, P, k, k + 2 + R1));
+      TRY(launch_cgs2_update(ctx, P, k));
+      continue;
+    }
     if (ctx->world > 1) TRY(halo_exchange(ctx, HV_V, k));
     // rev = 0: alternating the walk direction per kernel (to reuse the
     // previous kernel's L2 tail) measured slower on B200 (tools/prof_by_k.py)
     StepEpi se{k};
-    TRY(launch_spmv(ctx, A, P, se, m + 1, (uint32_t)k, 0));
+    TRY(launch_spmv(ctx, A, P, se, m + 1, (uint32_t)k));
     TRY(finish_global<100>(ctx, P, k, k + 1));
     TRY(launch_cgs2_b(ctx, P, k, k + 2 + R1, 0, ctx->cur_defl ? ctx->h_dstate->r : R1));
     TRY(finish_global<SW_CGS2_B>(ctx, P, k, k + 2 + R1));
@@ -894,6 +936,22 @@ Status matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags, pgm
     k_csr_to_sell<<<(unsigned)blocks, threads, 0, st>>>(M->view(), M->val, M->col, M->rp, cstage,
                                                         M->vstage, M->col_shift, M->nslices, 1);
   e = cudaGetLastError();
+  M->t_lo_end = 0;
+  M->t_hi_begin = M->ntiles;
+  if (e == cudaSuccess && ctx->world > 1 && a->n > 0) {
+    int h[2] = {-1, (int)a->n};
+    int* dh = nullptr;
+    e = cudaMalloc(&dh, sizeof(h));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dh, h, sizeof(h), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+      k_halo_rows<<<ctx->nsm * 4, 256, 0, st>>>(M->rp, cstage, (int)a->n, ctx->part.row_begin,
+                                                ctx->part.row_end, dh);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, dh, sizeof(h), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(dh);
+    M->t_lo_end = (h[0] + 1 + TILE - 1) / TILE;
+    M->t_hi_begin = std::max(M->t_lo_end, h[1] / TILE);
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   cudaFree(cstage);
   if (e != cudaSuccess)
@@ -949,8 +1007,9 @@ double* halo_vec(pgm_context* ctx, HaloKind kind, int slot) {
 // [0, halo) go down into the lower neighbour's halo_hi region and own rows
 // [n - halo, n) go up into the upper neighbour's halo_lo region (slabs are at
 // least two planes thick, so halos only ever come from adjacent ranks).
-Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot) {
+Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot, cudaStream_t st) {
   if (ctx->world == 1) return {};
+  if (!st) st = ctx->stream;
   double* vec = halo_vec(ctx, kind, slot);
   const size_t lo = ctx->lo, hi = ctx->hi, n = ctx->n;
   const int below = ctx->rank - 1, above = ctx->rank + 1;
@@ -961,14 +1020,14 @@ Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot) {
     if (below >= 0 && lo > 0) {
       pgm_context* nb = L->ctx[below];
       const double* src = halo_vec(nb, kind, slot) + nb->lo + nb->n - nb->hi;
-      CU(cudaMemcpyAsync(vec, src, 8 * lo, cudaMemcpyDeviceToDevice, ctx->stream));
+      CU(cudaMemcpyAsync(vec, src, 8 * lo, cudaMemcpyDeviceToDevice, st));
     }
     if (above < ctx->world && hi > 0) {
       pgm_context* na = L->ctx[above];
       const double* src = halo_vec(na, kind, slot) + na->lo;
-      CU(cudaMemcpyAsync(vec + lo + n, src, 8 * hi, cudaMemcpyDeviceToDevice, ctx->stream));
+      CU(cudaMemcpyAsync(vec + lo + n, src, 8 * hi, cudaMemcpyDeviceToDevice, st));
     }
-    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaStreamSynchronize(st));
     L->barrier();
     return {};
   }
@@ -976,12 +1035,12 @@ Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot) {
   if (nccl_lite::group_start() != 0) return Status{PGM_ENCCL, "ncclGroupStart failed"};
   int rc = 0;
   if (below >= 0 && lo > 0) {
-    rc |= nccl_lite::send_f64(vec + lo, lo, below, ctx->nccl, ctx->stream);
-    rc |= nccl_lite::recv_f64(vec, lo, below, ctx->nccl, ctx->stream);
+    rc |= nccl_lite::send_f64(vec + lo, lo, below, ctx->nccl, st);
+    rc |= nccl_lite::recv_f64(vec, lo, below, ctx->nccl, st);
   }
   if (above < ctx->world && hi > 0) {
-    rc |= nccl_lite::send_f64(vec + lo + n - hi, hi, above, ctx->nccl, ctx->stream);
-    rc |= nccl_lite::recv_f64(vec + lo + n, hi, above, ctx->nccl, ctx->stream);
+    rc |= nccl_lite::send_f64(vec + lo + n - hi, hi, above, ctx->nccl, st);
+    rc |= nccl_lite::recv_f64(vec + lo + n, hi, above, ctx->nccl, st);
   }
   rc |= nccl_lite::group_end();
   if (rc) return Status{PGM_ENCCL, "halo exchange failed"};
@@ -1075,6 +1134,11 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) 
   if (e != cudaSuccess) return bail(Status{PGM_ECUDA, std::string("stream: ") + cudaGetErrorString(e)});
   cudaEventCreate(&ctx->ev0);
   cudaEventCreate(&ctx->ev1);
+  if (ctx->world > 1) {
+    cudaStreamCreateWithFlags(&ctx->hstream, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ctx->ev_halo_src, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->ev_halo_done, cudaEventDisableTiming);
+  }
   Status s;
   if ((s = dalloc(&ctx->g, 1)).code) return bail(s);
   if ((e = cudaMallocHost(&ctx->h_dstate, sizeof(DState))) != cudaSuccess)
@@ -1136,6 +1200,9 @@ void pgm_context_destroy(pgm_context* ctx) {
   if (ctx->h_dstate) cudaFreeHost(ctx->h_dstate);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->ev_halo_src) cudaEventDestroy(ctx->ev_halo_src);
+  if (ctx->ev_halo_done) cudaEventDestroy(ctx->ev_halo_done);
+  if (ctx->hstream) cudaStreamDestroy(ctx->hstream);
   if (ctx->nccl) nccl_lite::comm_destroy(ctx->nccl);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
