@@ -16,6 +16,8 @@
 
 #include <math.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "finish.cuh"
 #include "tma.cuh"
@@ -30,6 +32,8 @@ struct Sell {
   const unsigned short* lane_row;  // [nslices * 32] row within tile, 0xFFFF = empty lane
   const double* val;
   const unsigned* col;             // local column (index into the padded x buffer)
+  const unsigned short* col16;     // compressed: 16-bit column deltas (same entry layout)
+  const unsigned* lane_base;       // compressed: first column of the lane's row
   int ntiles;
   int n;
   int rev;  // walk the tiles from the last one (L2 reuse of the previous kernel's tail)
@@ -39,8 +43,14 @@ struct Sell {
 // so each lane reads 4 consecutive column ids (one uint4) and 4 values (two
 // double2) per group: every warp load instruction moves a contiguous 512 B or
 // 1 KB block.  Slice lengths are padded to a multiple of 4.
+// C16: column ids stored as 16-bit deltas to the previous entry of the row
+// (first entry: delta 0 from lane_base), 8 B per 4 entries instead of 16 B:
+// 10 instead of 12 bytes per nonzero.  Used when every delta of the matrix
+// fits (columns ascending, gaps < 65536: all z-slab meshes up to n_e = 127).
+template <bool C16>
 __device__ __forceinline__ void spmv_tile(const Sell& A, const double* __restrict__ x, int tile,
                                           double* ys) {
+  using CT = typename std::conditional<C16, uint2, uint4>::type;
   constexpr int UG = SPMV_UNROLL / 4;  // 4-entry groups in flight per lane
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
@@ -55,17 +65,22 @@ __device__ __forceinline__ void spmv_tile(const Sell& A, const double* __restric
     // prefetched ahead of the PDL wait (k_spmv).
     if (sl != warp || !PGM_SPMV_EARLY_PF) {
       if (lane == 0) tma_prefetch_l2(A.val + base, (uint32_t)L4 * 128u * 8u);
-      if (lane == 1) tma_prefetch_l2(A.col + base, (uint32_t)L4 * 128u * 4u);
+      if (lane == 1) {
+        if (C16) tma_prefetch_l2(A.col16 + base, (uint32_t)L4 * 128u * 2u);
+        else tma_prefetch_l2(A.col + base, (uint32_t)L4 * 128u * 4u);
+      }
     }
 #endif
     const int len = (int)A.lane_len[s * 32 + lane];
     const unsigned short ro = A.lane_row[s * 32 + lane];
-    const uint4* cp = reinterpret_cast<const uint4*>(A.col + base) + lane;
+    const CT* cp = C16 ? reinterpret_cast<const CT*>(A.col16 + base) + lane
+                       : reinterpret_cast<const CT*>(A.col + base) + lane;
+    unsigned prev = C16 ? A.lane_base[s * 32 + lane] : 0u;
     const double2* vp = reinterpret_cast<const double2*>(A.val + base) + 2 * lane;
     double acc = 0.0;
     // software pipeline: the streaming loads of group g+UG are in flight while
     // the x gathers and the accumulation of group g run
-    uint4 c[UG];
+    CT c[UG];
     double2 va[UG], vb[UG];
 #pragma unroll
     for (int u = 0; u < UG; ++u) {
@@ -76,7 +91,7 @@ __device__ __forceinline__ void spmv_tile(const Sell& A, const double* __restric
       }
     }
     for (int g = 0; g < L4; g += UG) {
-      uint4 cn[UG];
+      CT cn[UG];
       double2 van[UG], vbn[UG];
 #pragma unroll
       for (int u = 0; u < UG; ++u) {
@@ -90,10 +105,23 @@ __device__ __forceinline__ void spmv_tile(const Sell& A, const double* __restric
 #pragma unroll
       for (int u = 0; u < UG; ++u) {
         const int t = (g + u) * 4;
-        xv[u][0] = (t + 0 < len) ? __ldg(x + c[u].x) : 0.0;
-        xv[u][1] = (t + 1 < len) ? __ldg(x + c[u].y) : 0.0;
-        xv[u][2] = (t + 2 < len) ? __ldg(x + c[u].z) : 0.0;
-        xv[u][3] = (t + 3 < len) ? __ldg(x + c[u].w) : 0.0;
+        unsigned c0, c1, c2, c3;
+        if constexpr (C16) {
+          c0 = prev + (c[u].x & 0xFFFFu);
+          c1 = c0 + (c[u].x >> 16);
+          c2 = c1 + (c[u].y & 0xFFFFu);
+          c3 = c2 + (c[u].y >> 16);
+          prev = c3;
+        } else {
+          c0 = c[u].x;
+          c1 = c[u].y;
+          c2 = c[u].z;
+          c3 = c[u].w;
+        }
+        xv[u][0] = (t + 0 < len) ? __ldg(x + c0) : 0.0;
+        xv[u][1] = (t + 1 < len) ? __ldg(x + c1) : 0.0;
+        xv[u][2] = (t + 2 < len) ? __ldg(x + c2) : 0.0;
+        xv[u][3] = (t + 3 < len) ? __ldg(x + c3) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < UG; ++u) {
@@ -333,7 +361,7 @@ struct SpmvSeg {
   int b0, len0, b1;
 };
 
-template <class Epi, bool SEG>
+template <class Epi, bool SEG, bool C16>
 __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params P, Epi E,
                                                                  SpmvSeg sg) {
   extern __shared__ double sm[];
@@ -353,7 +381,10 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
       const unsigned long long base = A.sptr[sidx];
       const uint32_t L4 = (uint32_t)((A.sptr[sidx + 1] - base) >> 7);
       if (L4 > 0 && ln == 0) tma_prefetch_l2(A.val + base, L4 * 128u * 8u);
-      if (L4 > 0 && ln == 1) tma_prefetch_l2(A.col + base, L4 * 128u * 4u);
+      if (L4 > 0 && ln == 1) {
+        if (C16) tma_prefetch_l2(A.col16 + base, L4 * 128u * 2u);
+        else tma_prefetch_l2(A.col + base, L4 * 128u * 4u);
+      }
     }
   }
 #endif
@@ -371,7 +402,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
   const double* x = epi_input(P, E);
   // exactly one tile per block (grid = ntiles): the epilogue accumulators are
   // only live after the SpMV part, which keeps the SpMV loop's registers low
-  spmv_tile(A, x, tile, ys);
+  spmv_tile<C16>(A, x, tile, ys);
   __syncthreads();
   double acc[NVL];
 #pragma unroll
@@ -1226,6 +1257,50 @@ __global__ void k_observe(DState* d, double v) {
 
 // ---------------------------------------------------------------------------
 // CSR -> SELL conversion: one warp per slice.
+// 16-bit column-delta compression of a SELL matrix (see spmv_tile<true>).
+// k_sell_delta_max: largest delta between consecutive entries of a row
+// (unsigned: a descending pair counts as huge and disables compression).
+__global__ void k_sell_delta_max(Sell A, int nslices, unsigned* out) {
+  const int lane = threadIdx.x & 31;
+  const size_t s = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  if (s >= (size_t)nslices) return;
+  const unsigned long long base = A.sptr[s];
+  const int len = (int)A.lane_len[s * 32 + lane];
+  unsigned m = 0, prev = 0;
+  for (int t = 0; t < len; ++t) {
+    const unsigned c = A.col[base + (size_t)(t >> 2) * 128 + lane * 4 + (t & 3)];
+    if (t > 0) m = max(m, c - prev);
+    prev = c;
+  }
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 16));
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 8));
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 4));
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  if (lane == 0) atomicMax(out, m);
+}
+
+__global__ void k_sell_compress(Sell A, int nslices, unsigned short* col16, unsigned* lane_base) {
+  const int lane = threadIdx.x & 31;
+  const size_t s = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  if (s >= (size_t)nslices) return;
+  const unsigned long long base = A.sptr[s];
+  const int L = (int)((A.sptr[s + 1] - base) >> 5);
+  const int len = (int)A.lane_len[s * 32 + lane];
+  unsigned prev = len > 0 ? A.col[base + lane * 4] : 0u;
+  lane_base[s * 32 + lane] = prev;
+  for (int t = 0; t < L; ++t) {
+    const size_t idx = base + (size_t)(t >> 2) * 128 + lane * 4 + (t & 3);
+    unsigned d = 0;
+    if (t < len) {
+      const unsigned c = A.col[idx];
+      d = c - prev;
+      prev = c;
+    }
+    col16[idx] = (unsigned short)d;
+  }
+}
+
 // Rows that read halo columns (global column < rb or >= re; columns ascending
 // per row): out[0] = last such row below, out[1] = first such row above.
 __global__ void k_halo_rows(const unsigned* rp, const unsigned* col, int n, unsigned rb,

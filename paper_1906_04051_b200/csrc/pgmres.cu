@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
@@ -162,6 +163,8 @@ struct pgm_matrix {
   unsigned short* lane_row = nullptr;
   double* val = nullptr;
   unsigned* col = nullptr;
+  unsigned short* col16 = nullptr;  // 16-bit column deltas (col freed when set)
+  unsigned* lane_base = nullptr;
   unsigned* rp = nullptr;      // device CSR row_ptr (kept for value updates)
   double* vstage = nullptr;    // device CSR values staging
   unsigned col_shift = 0;
@@ -175,6 +178,8 @@ struct pgm_matrix {
     S.lane_row = lane_row;
     S.val = val;
     S.col = col;
+    S.col16 = col16;
+    S.lane_base = lane_base;
     S.ntiles = ntiles;
     S.n = (int)n;
     S.rev = 0;
@@ -297,7 +302,17 @@ uint32_t prof_class_sweep() {
 size_t spmv_smem(int nv) { return sizeof(double) * spmv_smem_doubles(nv); }
 
 // seg: 0 = every tile; 1 = interior tiles; 2 = halo-reading boundary tiles
-// (1 and 2 together form one reduction over all tiles, world > 1).
+// (1 and 2 together form one reduction over all tiles, world > 1; step SpMV only).
+template <class Epi, bool SEG, bool C16>
+Status launch_spmv_k(pgm_context* ctx, int G, size_t smem, const Sell& sv, const Params& P,
+                     const Epi& E, const SpmvSeg& sg) {
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_spmv<Epi, SEG, C16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  CU(launch_pdl(ctx, k_spmv<Epi, SEG, C16>, G, SPMV_THREADS, smem, sv, P, E, sg));
+  return {};
+}
+
 template <class Epi>
 Status launch_spmv(pgm_context* ctx, const pgm_matrix* A, const Params& P, const Epi& E,
                    int nvmax, uint32_t prof_k = 0, int seg = 0) {
@@ -315,15 +330,20 @@ Status launch_spmv(pgm_context* ctx, const pgm_matrix* A, const Params& P, const
   if (G <= 0) return {};
   ProfScope ps(ctx, prof_class_of<Epi>(), prof_k);
   // one tile per block: the hardware scheduler balances the tiles
-  if (seg == 0) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_spmv<Epi, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    CU(launch_pdl(ctx, k_spmv<Epi, false>, G, SPMV_THREADS, smem, sv, P, E, sg));
-  } else {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_spmv<Epi, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    CU(launch_pdl(ctx, k_spmv<Epi, true>, G, SPMV_THREADS, smem, sv, P, E, sg));
+  const bool c16 = A->col16 != nullptr;
+  if constexpr (std::is_same<Epi, StepEpi>::value) {
+    if (seg != 0) {
+      const Status st = c16 ? launch_spmv_k<Epi, true, true>(ctx, G, smem, sv, P, E, sg)
+                            : launch_spmv_k<Epi, true, false>(ctx, G, smem, sv, P, E, sg);
+      TRY(st);
+      ctx->launches++;
+      CU(cudaGetLastError());
+      return {};
+    }
   }
+  const Status st = c16 ? launch_spmv_k<Epi, false, true>(ctx, G, smem, sv, P, E, sg)
+                        : launch_spmv_k<Epi, false, false>(ctx, G, smem, sv, P, E, sg);
+  TRY(st);
   ctx->launches++;
   CU(cudaGetLastError());
   return {};
@@ -936,6 +956,36 @@ Status matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags, pgm
     k_csr_to_sell<<<(unsigned)blocks, threads, 0, st>>>(M->view(), M->val, M->col, M->rp, cstage,
                                                         M->vstage, M->col_shift, M->nslices, 1);
   e = cudaGetLastError();
+  if (e == cudaSuccess && M->nslices > 0 && !std::getenv("PGMRES_NO_C16")) {
+    // 16-bit column deltas when every gap fits (10 instead of 12 B / nonzero)
+    unsigned* dm = nullptr;
+    unsigned hm = 0;
+    e = cudaMalloc(&dm, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemsetAsync(dm, 0, sizeof(unsigned), st);
+    if (e == cudaSuccess) k_sell_delta_max<<<(unsigned)blocks, threads, 0, st>>>(M->view(), M->nslices, dm);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hm, dm, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(dm);
+    if (e == cudaSuccess && hm <= 0xFFFFu) {
+      if (cudaMalloc(&M->col16, 2 * M->stored) == cudaSuccess &&
+          cudaMalloc(&M->lane_base, 4 * (size_t)M->nslices * 32) == cudaSuccess) {
+        Sell v32 = M->view();
+        v32.col16 = nullptr;
+        k_sell_compress<<<(unsigned)blocks, threads, 0, st>>>(v32, M->nslices, M->col16,
+                                                              M->lane_base);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess) {
+          cudaFree(M->col);
+          M->col = nullptr;
+        }
+      } else {
+        cudaGetLastError();  // not enough memory: keep 32-bit columns
+        if (M->col16) cudaFree(M->col16);
+        M->col16 = nullptr;
+      }
+    }
+  }
   M->t_lo_end = 0;
   M->t_hi_begin = M->ntiles;
   if (e == cudaSuccess && ctx->world > 1 && a->n > 0) {
@@ -1264,6 +1314,8 @@ void pgm_matrix_destroy(pgm_matrix* a) {
   dfree(a->lane_row);
   dfree(a->val);
   dfree(a->col);
+  dfree(a->col16);
+  dfree(a->lane_base);
   dfree(a->rp);
   dfree(a->vstage);
   delete a;
