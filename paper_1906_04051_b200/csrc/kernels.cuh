@@ -404,6 +404,64 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
   // only live after the SpMV part, which keeps the SpMV loop's registers low
   spmv_tile<C16>(A, x, tile, ys);
   __syncthreads();
+  if constexpr (std::is_same<Epi, StepEpi>::value) {
+    // Step epilogue, two phases.  (1) y = s_k (A W_k) + AU c -> W_{k+1} and
+    // ys, thread per row.  (2) pass-1 dots W_l . y: warp w owns the basis
+    // vectors l = w, w + 8, ... and streams its 512 rows with 16 independent
+    // loads per lane; one warp sum per vector, no cross-warp combine.
+    const int k = E.k;
+    const int r = P.d->r;
+    const size_t ld = P.ld;
+    const int row0 = tile * TILE;
+    const int rows = min(TILE, A.n - row0);
+    double* wnext = P.V + (size_t)(k + 1) * ld + P.lo + row0;
+    const double* au0 = P.AU + P.lo + row0;
+    for (int i = threadIdx.x; i < TILE; i += SPMV_THREADS) {
+      double y = 0.0;
+      if (i < rows) {
+        y = small[0] * ys[i];
+        int l = 0;
+        for (; l + 1 < r; l += 2) {
+          const double t0 = __ldg(au0 + (size_t)l * ld + i);
+          const double t1 = __ldg(au0 + (size_t)(l + 1) * ld + i);
+          y += small[1 + l] * t0;
+          y += small[2 + l] * t1;
+        }
+        if (l < r) y += small[1 + l] * __ldg(au0 + (size_t)l * ld + i);
+        wnext[i] = y;
+      }
+      ys[i] = y;
+    }
+    __syncthreads();
+    const int np = k + 1;
+    const double* v0 = P.V + P.lo + row0;
+    for (int l = warp; l < np; l += SPMV_WARPS) {
+      const double* v = v0 + (size_t)l * ld + lane;
+      double a[4] = {0.0, 0.0, 0.0, 0.0};
+      if (rows == TILE) {
+        double t[TILE / 32];
+#pragma unroll
+        for (int q = 0; q < TILE / 32; ++q) t[q] = __ldg(v + 32 * q);
+#pragma unroll
+        for (int q = 0; q < TILE / 32; ++q) a[q & 3] += t[q] * ys[lane + 32 * q];
+      } else {
+        for (int q = 0; q < TILE / 32; ++q)
+          if (lane + 32 * q < rows) a[q & 3] += __ldg(v + 32 * q) * ys[lane + 32 * q];
+      }
+      const double sum = warp_sum((a[0] + a[1]) + (a[2] + a[3]));
+      if (lane == 0) bvals[l] = sum;
+    }
+    pdl_trigger();
+    __syncthreads();
+    const int G = SEG ? A.ntiles : (int)gridDim.x;
+    if (P.world > 1) {
+      if (grid_reduce_ex(bvals, nv, P, red, G, tile))
+        for (int v = threadIdx.x; v < nv; v += blockDim.x) P.red_out[v] = red[v];
+      return;
+    }
+    if (grid_reduce_ex(bvals, nv, P, red, G, tile)) E.finish(P, red);
+    return;
+  }
   double acc[NVL];
 #pragma unroll
   for (int s = 0; s < NVL; ++s) acc[s] = 0.0;
