@@ -18,6 +18,8 @@
 
 #include <type_traits>
 
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 #include "finish.cuh"
 #include "tma.cuh"
@@ -1315,6 +1317,57 @@ __global__ void k_observe(DState* d, double v) {
 
 // ---------------------------------------------------------------------------
 // CSR -> SELL conversion: one warp per slice.
+// SELL layout of one 512-row tile (one block): stable sort of the rows by
+// length, descending (cub::BlockRadixSort is stable; padding rows past n sort
+// after every real row), 32 rows per slice.  Writes lane_len / lane_row and
+// the slice sizes into sptr[s] (32 * length rounded up to a multiple of 4;
+// exclusive-scanned afterwards).  bad: bit 0 = row_ptr[0] != 0 or
+// row_ptr[n] != nnz, bit 1 = row_ptr decreasing.
+__global__ void __launch_bounds__(256) k_sell_layout(const unsigned* rp, int n,
+                                                     unsigned long long nnz, unsigned* lane_len,
+                                                     unsigned short* lane_row,
+                                                     unsigned long long* sptr, int* bad) {
+  using Sort = cub::BlockRadixSort<unsigned, 256, 2, int>;
+  __shared__ typename Sort::TempStorage tmp;
+  __shared__ unsigned s_len[TILE];
+  const int tile = blockIdx.x;
+  const int r0 = tile * TILE;
+  unsigned key[2];
+  int val[2];
+  for (int q = 0; q < 2; ++q) {
+    const int i = threadIdx.x * 2 + q;  // blocked arrangement: keeps the original order
+    const int row = r0 + i;
+    unsigned len = 0;
+    if (row < n) {
+      const unsigned a = rp[row], b = rp[row + 1];
+      if (b < a) atomicOr(bad, 2);
+      len = b - a;
+    }
+    // descending by length; padding rows get the lowest key (after empty rows)
+    key[q] = row < n ? len + 1u : 0u;
+    val[q] = i;
+  }
+  if (tile == 0 && threadIdx.x == 0 && (rp[0] != 0u || (unsigned long long)rp[n] != nnz))
+    atomicOr(bad, 1);
+  Sort(tmp).SortDescending(key, val);
+  for (int q = 0; q < 2; ++q) {
+    const int j = threadIdx.x * 2 + q;  // sorted position = slice * 32 + lane
+    const int row = r0 + val[q];
+    const bool real = key[q] != 0u;
+    const unsigned len = real ? key[q] - 1u : 0u;
+    lane_len[(size_t)tile * TILE + j] = len;
+    lane_row[(size_t)tile * TILE + j] = real ? (unsigned short)val[q] : (unsigned short)0xFFFF;
+    s_len[j] = len;
+    (void)row;
+  }
+  __syncthreads();
+  if (threadIdx.x < SPT) {
+    unsigned m = 0;
+    for (int l = 0; l < 32; ++l) m = max(m, s_len[threadIdx.x * 32 + l]);
+    sptr[(size_t)tile * SPT + threadIdx.x] = 32ull * ((m + 3u) / 4u * 4u);
+  }
+}
+
 // 16-bit column-delta compression of a SELL matrix (see spmv_tile<true>).
 // k_sell_delta_max: largest delta between consecutive entries of a row
 // (unsigned: a descending pair counts as huge and disables compression).

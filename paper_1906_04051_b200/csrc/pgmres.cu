@@ -72,6 +72,28 @@ void dfree(T*& p) {
   p = nullptr;
 }
 
+// Stream-ordered allocations for the per-matrix arrays (the pool keeps freed
+// memory, so the e2e path's upload/destroy per solve does not pay cudaMalloc /
+// cudaFree synchronisation).
+template <class T>
+Status dalloc_async(T** p, size_t count, cudaStream_t st) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return Status{PGM_ENOMEM, std::string("cudaMallocAsync(") +
+                                  std::to_string(count * sizeof(T)) + " B): " +
+                                  cudaGetErrorString(e)};
+  }
+  return {};
+}
+template <class T>
+void dfree_async(T*& p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+  p = nullptr;
+}
+
 size_t round_up(size_t a, size_t b) { return (a + b - 1) / b * b; }
 
 }  // namespace
@@ -854,100 +876,74 @@ Status solve_impl(pgm_context* ctx, pgm_matrix* A, pgm_deflator* dflt, const dou
 }
 
 // ---------------------------------------------------------------------------
-// Matrix upload: CSR (owned rows, global columns) -> SELL-32 tiles.
-struct SliceLayout {
-  std::vector<unsigned long long> sptr;
-  std::vector<unsigned> lane_len;
-  std::vector<unsigned short> lane_row;
-};
-
-SliceLayout build_layout(const uint32_t* rp, uint32_t n) {
-  SliceLayout L;
-  const int ntiles = (int)((n + TILE - 1) / TILE);
-  const size_t nslices = (size_t)ntiles * SPT;
-  L.sptr.assign(nslices + 1, 0);
-  L.lane_len.assign(nslices * 32, 0);
-  L.lane_row.assign(nslices * 32, 0xFFFF);
-  std::vector<int> order(TILE);
-  unsigned long long off = 0;
-  for (int t = 0; t < ntiles; ++t) {
-    const uint32_t r0 = (uint32_t)t * TILE;
-    const int rows = (int)std::min<uint32_t>(TILE, n - r0);
-    for (int i = 0; i < rows; ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.begin() + rows, [&](int a, int b) {
-      return (rp[r0 + a + 1] - rp[r0 + a]) > (rp[r0 + b + 1] - rp[r0 + b]);
-    });
-    for (int sl = 0; sl < SPT; ++sl) {
-      const size_t s = (size_t)t * SPT + sl;
-      unsigned Lmax = 0;
-      for (int lane = 0; lane < 32; ++lane) {
-        const int idx = sl * 32 + lane;
-        if (idx < rows) {
-          const int row = order[idx];
-          const unsigned len = rp[r0 + row + 1] - rp[r0 + row];
-          L.lane_len[s * 32 + lane] = len;
-          L.lane_row[s * 32 + lane] = (unsigned short)row;
-          Lmax = std::max(Lmax, len);
-        }
-      }
-      L.sptr[s] = off;
-      off += 32ull * ((Lmax + 3) / 4 * 4);  // 4-deep interleave (uint4 / double2 loads)
-    }
-  }
-  L.sptr[nslices] = off;
-  return L;
-}
-
+// Matrix upload: CSR (owned rows, global columns) -> SELL-32 tiles, layout
+// built on the device (k_sell_layout: per-tile stable sort by row length).
 Status matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags, pgm_matrix** out) {
   if (!a || !out) return einval("pgm_matrix_upload: null argument");
   if (a->n != ctx->n)
     return einval("pgm_matrix_upload: view has " + std::to_string(a->n) + " rows, partition owns " +
                   std::to_string(ctx->n));
   const bool dev = (flags & PGM_DEVICE_PTRS) != 0;
-  std::vector<uint32_t> rp_h(a->n + 1);
-  if (dev) {
-    CU(cudaMemcpy(rp_h.data(), a->row_ptr, 4 * (a->n + 1), cudaMemcpyDeviceToHost));
-  } else {
-    std::memcpy(rp_h.data(), a->row_ptr, 4 * (a->n + 1));
-  }
-  if (rp_h[0] != 0 || rp_h[a->n] != a->nnz)
-    return einval("pgm_matrix_upload: row_ptr must start at 0 and end at nnz");
-  for (uint32_t i = 0; i < a->n; ++i)
-    if (rp_h[i + 1] < rp_h[i]) return einval("pgm_matrix_upload: row_ptr not monotone");
-  SliceLayout L = build_layout(rp_h.data(), a->n);
+  cudaStream_t st = ctx->stream;
   auto* M = new pgm_matrix();
   M->ctx = ctx;
   M->n = a->n;
   M->nnz = a->nnz;
   M->ntiles = (int)((a->n + TILE - 1) / TILE);
   M->nslices = M->ntiles * SPT;
-  M->stored = L.sptr.back();
   M->col_shift = ctx->part.row_begin - ctx->part.halo_lo;
   auto cleanup = [&](Status s) {
+    cudaStreamSynchronize(st);
     pgm_matrix_destroy(M);
     return s;
   };
   Status s;
-  if ((s = dalloc(&M->sptr, L.sptr.size())).code) return cleanup(s);
-  if ((s = dalloc(&M->lane_len, L.lane_len.size())).code) return cleanup(s);
-  if ((s = dalloc(&M->lane_row, L.lane_row.size())).code) return cleanup(s);
-  if ((s = dalloc(&M->val, M->stored)).code) return cleanup(s);
-  if ((s = dalloc(&M->col, M->stored)).code) return cleanup(s);
-  if ((s = dalloc(&M->rp, (size_t)a->n + 1)).code) return cleanup(s);
-  if ((s = dalloc(&M->vstage, a->nnz)).code) return cleanup(s);
-  unsigned* cstage = nullptr;
-  if ((s = dalloc(&cstage, a->nnz)).code) return cleanup(s);
   const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  cudaStream_t st = ctx->stream;
   cudaError_t e = cudaSuccess;
-  e = e ? e : cudaMemcpyAsync(M->sptr, L.sptr.data(), 8 * L.sptr.size(), cudaMemcpyHostToDevice, st);
-  e = e ? e : cudaMemcpyAsync(M->lane_len, L.lane_len.data(), 4 * L.lane_len.size(), cudaMemcpyHostToDevice, st);
-  e = e ? e : cudaMemcpyAsync(M->lane_row, L.lane_row.data(), 2 * L.lane_row.size(), cudaMemcpyHostToDevice, st);
-  e = e ? e : cudaMemcpyAsync(M->rp, rp_h.data(), 4 * ((size_t)a->n + 1), cudaMemcpyHostToDevice, st);
+  // row_ptr checks (start 0, end nnz, monotone) on the device copy
+  if ((s = dalloc_async(&M->rp, (size_t)a->n + 1, st)).code) return cleanup(s);
+  e = cudaMemcpyAsync(M->rp, a->row_ptr, 4 * ((size_t)a->n + 1), kind, st);
+  const size_t ns = (size_t)M->nslices;
+  if ((s = dalloc_async(&M->sptr, ns + 1, st)).code) return cleanup(s);
+  if ((s = dalloc_async(&M->lane_len, ns * 32, st)).code) return cleanup(s);
+  if ((s = dalloc_async(&M->lane_row, ns * 32, st)).code) return cleanup(s);
+  int* dbad = nullptr;
+  void* dtmp = nullptr;
+  size_t tmp_bytes = 0;
+  if ((s = dalloc_async(&dbad, 1, st)).code) return cleanup(s);
+  e = e ? e : cudaMemsetAsync(dbad, 0, sizeof(int), st);
+  if (e == cudaSuccess && M->ntiles > 0) {
+    k_sell_layout<<<M->ntiles, 256, 0, st>>>(M->rp, (int)a->n, (unsigned long long)a->nnz,
+                                             M->lane_len, M->lane_row, M->sptr, dbad);
+    e = cudaGetLastError();
+  }
+  // sptr = exclusive scan of the slice sizes (k_sell_layout wrote them to sptr[s])
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, M->sptr, M->sptr, (int)(ns + 1), st);
+  if ((s = dalloc_async((char**)&dtmp, tmp_bytes, st)).code) return cleanup(s);
+  e = e ? e : cudaMemsetAsync(M->sptr + ns, 0, sizeof(unsigned long long), st);
+  if (e == cudaSuccess)
+    e = cub::DeviceScan::ExclusiveSum(dtmp, tmp_bytes, M->sptr, M->sptr, (int)(ns + 1), st);
+  unsigned long long stored = 0;
+  int bad = 0;
+  e = e ? e : cudaMemcpyAsync(&stored, M->sptr + ns, 8, cudaMemcpyDeviceToHost, st);
+  e = e ? e : cudaMemcpyAsync(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, st);
+  e = e ? e : cudaStreamSynchronize(st);
+  cudaFreeAsync(dtmp, st);
+  cudaFreeAsync(dbad, st);
+  if (e != cudaSuccess)
+    return cleanup(Status{PGM_ECUDA, std::string("upload layout: ") + cudaGetErrorString(e)});
+  if (bad & 1) return cleanup(einval("pgm_matrix_upload: row_ptr must start at 0 and end at nnz"));
+  if (bad & 2) return cleanup(einval("pgm_matrix_upload: row_ptr not monotone"));
+  M->stored = stored;
+  if ((s = dalloc_async(&M->val, M->stored, st)).code) return cleanup(s);
+  if ((s = dalloc_async(&M->col, M->stored, st)).code) return cleanup(s);
+  if ((s = dalloc_async(&M->vstage, a->nnz, st)).code) return cleanup(s);
+  unsigned* cstage = nullptr;
+  if ((s = dalloc_async(&cstage, a->nnz, st)).code) return cleanup(s);
   e = e ? e : cudaMemcpyAsync(M->vstage, a->values, 8 * a->nnz, kind, st);
   e = e ? e : cudaMemcpyAsync(cstage, a->col_idx, 4 * a->nnz, kind, st);
   if (e != cudaSuccess) {
-    cudaFree(cstage);
+    cudaFreeAsync(cstage, st);
     return cleanup(Status{PGM_ECUDA, std::string("upload: ") + cudaGetErrorString(e)});
   }
   const int threads = 256;
@@ -960,29 +956,26 @@ Status matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags, pgm
     // 16-bit column deltas when every gap fits (10 instead of 12 B / nonzero)
     unsigned* dm = nullptr;
     unsigned hm = 0;
-    e = cudaMalloc(&dm, sizeof(unsigned));
+    e = cudaMallocAsync(reinterpret_cast<void**>(&dm), sizeof(unsigned), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(dm, 0, sizeof(unsigned), st);
     if (e == cudaSuccess) k_sell_delta_max<<<(unsigned)blocks, threads, 0, st>>>(M->view(), M->nslices, dm);
     if (e == cudaSuccess) e = cudaMemcpyAsync(&hm, dm, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    cudaFree(dm);
+    cudaFreeAsync(dm, st);
     if (e == cudaSuccess && hm <= 0xFFFFu) {
-      if (cudaMalloc(&M->col16, 2 * M->stored) == cudaSuccess &&
-          cudaMalloc(&M->lane_base, 4 * (size_t)M->nslices * 32) == cudaSuccess) {
+      if (cudaMallocAsync(reinterpret_cast<void**>(&M->col16), 2 * M->stored, st) == cudaSuccess &&
+          cudaMallocAsync(reinterpret_cast<void**>(&M->lane_base), 4 * (size_t)M->nslices * 32,
+                          st) == cudaSuccess) {
         Sell v32 = M->view();
         v32.col16 = nullptr;
         k_sell_compress<<<(unsigned)blocks, threads, 0, st>>>(v32, M->nslices, M->col16,
                                                               M->lane_base);
         e = cudaGetLastError();
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e == cudaSuccess) {
-          cudaFree(M->col);
-          M->col = nullptr;
-        }
+        if (e == cudaSuccess) dfree_async(M->col, st);
       } else {
         cudaGetLastError();  // not enough memory: keep 32-bit columns
-        if (M->col16) cudaFree(M->col16);
-        M->col16 = nullptr;
+        dfree_async(M->col16, st);
+        dfree_async(M->lane_base, st);
       }
     }
   }
@@ -1002,8 +995,8 @@ Status matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags, pgm
     M->t_lo_end = (h[0] + 1 + TILE - 1) / TILE;
     M->t_hi_begin = std::max(M->t_lo_end, h[1] / TILE);
   }
+  cudaFreeAsync(cstage, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  cudaFree(cstage);
   if (e != cudaSuccess)
     return cleanup(Status{PGM_ECUDA, std::string("csr->sell: ") + cudaGetErrorString(e)});
   *out = M;
@@ -1180,6 +1173,13 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) 
   int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device);
   ctx->nsm = nsm > 0 ? nsm : 148;
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, cfg->device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;  // keep freed matrix arrays cached in the pool
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) return bail(Status{PGM_ECUDA, std::string("stream: ") + cudaGetErrorString(e)});
   cudaEventCreate(&ctx->ev0);
@@ -1309,15 +1309,16 @@ pgm_status pgm_matrix_update_values(pgm_matrix* a, const double* values, int32_t
 
 void pgm_matrix_destroy(pgm_matrix* a) {
   if (!a) return;
-  dfree(a->sptr);
-  dfree(a->lane_len);
-  dfree(a->lane_row);
-  dfree(a->val);
-  dfree(a->col);
-  dfree(a->col16);
-  dfree(a->lane_base);
-  dfree(a->rp);
-  dfree(a->vstage);
+  cudaStream_t st = a->ctx ? a->ctx->stream : nullptr;
+  dfree_async(a->sptr, st);
+  dfree_async(a->lane_len, st);
+  dfree_async(a->lane_row, st);
+  dfree_async(a->val, st);
+  dfree_async(a->col, st);
+  dfree_async(a->col16, st);
+  dfree_async(a->lane_base, st);
+  dfree_async(a->rp, st);
+  dfree_async(a->vstage, st);
   delete a;
 }
 
