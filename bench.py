@@ -148,10 +148,10 @@ def class_bytes(cls, n, nnz, k, r, steps):
     spmv = 12 * nnz + 4 * (n + 1) + 16 * n
     if cls == 0:
         return step_spmv_bytes(n, nnz, k, r)
-    if cls == 1:  # w1 = w - V h1 (read V_0..k, w; write w) ; dots from smem
-        return 8 * n * (k + 3)
-    if cls == 2:  # w2 = w1 - V h2, ||w2||, U^T w2
+    if cls == 1:  # pass B: w1 = w - V h1 (read V_0..k, w, U_0..r-1; write w); V^T w1, ||w1||, U^T w1
         return 8 * n * (k + 3 + r)
+    if cls == 2:  # pass C: w2 = w1 - V h2 (read V_0..k, w1; write w2), no reduction
+        return 8 * n * (k + 3)
     if cls == 3:  # x += V y + U c
         return 8 * n * (steps + r + 2)
     if cls == 8:  # r = b - A x, ||r||, U^T r
@@ -254,7 +254,7 @@ def run_gpu(a):
         e[0] += b
         e[1] += t_ms / 1e3
         e[2] += 1
-    names = {0: "step_spmv", 1: "cgs2_pass2_dots", 2: "cgs2_update_norm", 3: "x_update",
+    names = {0: "step_spmv", 1: "cgs2_passB_update_dots", 2: "cgs2_passC_update", 3: "x_update",
              4: "ritz", 5: "push_sweeps", 6: "push_spmv", 7: "rotate", 8: "residual_spmv",
              9: "other"}
     prof_total = float(ms.sum()) / 1e3
@@ -265,8 +265,18 @@ def run_gpu(a):
     peak, peak_kind = peaks()
     sp = per.get(0, [0, 1, 1])
     achieved = sp[0] / sp[1] / 1e9
+    traffic = None  # measured DRAM bytes per launch of this kernel (ncu, profiles/)
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp) and a.ne == 50 and a.m == 50 and world == 1:
+        with open(tp) as f:
+            traffic = json.load(f).get("k_spmv<StepEpi>", {}).get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None,
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "frac_dram": (round(traffic / (sp[1] / max(1, sp[2])) / 1e9 / peak, 4)
+                              if traffic else None),
+                "note": "achieved/frac use SURVEY 8(d) algorithmic bytes (12 B per nonzero); "
+                        "the kernel stores 16-bit column deltas (10 B), so frac_dram "
+                        "(ncu-measured DRAM bytes / launch time) is the physical fraction",
                 "kernel": "k_spmv<StepEpi> (SpMV + AU c deflation + CGS2 pass-1 dots)",
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "bytes_per_launch_avg": int(sp[0] / max(1, sp[2])),
