@@ -271,4 +271,70 @@ inline GmresReport gmres_restarted(const CsrMatrix& A, std::nullptr_t, const Den
   return detail::solve(A, b, x, cfg, nullptr, ex);
 }
 
+// ---- newton.hpp:15-54: the Newton driver, device-resident ------------------
+struct NewtonConfig {  // newton.hpp:15-23
+  std::uint32_t max_iters = 30;
+  double update_tol = 1e-8;
+  GmresConfig gmres{50, 100, 1e-10, false, 1e-14};
+  DeflationConfig deflation{};
+  bool use_deflation = true;
+  bool continuation = false;
+  std::uint32_t continuation_steps = 4;
+};
+
+struct NewtonIterRecord {  // newton.hpp:25-32
+  std::uint32_t iter;
+  double lambda;
+  double update_inf;
+  double residual_norm;
+  std::uint32_t gmres_restarts;
+  std::uint64_t gmres_inner;
+};
+
+struct NewtonReport {  // newton.hpp:34-43
+  std::vector<NewtonIterRecord> iters;
+  bool converged = false;
+  double final_residual = 0.0;
+  double final_update = 0.0;
+  std::uint64_t total_inner = 0;
+  double seconds = 0.0;
+};
+
+/// newton_solve(build_mesh(n_e), lambda, u, cfg, ex) for the Bratu problem:
+/// assembly, solves, update and norms on the GPU (pgm_newton_solve).  u is the
+/// global iterate (initial guess in, solution out).
+inline NewtonReport newton_solve(std::uint32_t n_e, double lambda, DenseVector& u,
+                                 const NewtonConfig& cfg, DeviceExecutor& ex) {
+  if (cfg.max_iters == 0) throw std::invalid_argument("newton: max_iters must be positive");
+  const std::size_t na = 2 * std::size_t(n_e) + 1;
+  if (u.size() != na * na * na) u.assign(na * na * na, 0.0);
+  pgm_context* ctx = ex.context(static_cast<index_t>(u.size()));
+  pgm_newton_config c{};
+  c.max_iters = cfg.max_iters;
+  c.update_tol = cfg.update_tol;
+  c.gmres = pgm_gmres_config{cfg.gmres.m, cfg.gmres.max_restarts, cfg.gmres.rel_tol,
+                             cfg.gmres.fixed_iterations ? 1 : 0, cfg.gmres.breakdown_scale};
+  c.deflation = pgm_deflation_config{cfg.deflation.r_max, cfg.deflation.drop,
+                                     cfg.deflation.accept_tol, cfg.deflation.inv_power_maxit,
+                                     cfg.deflation.inv_power_tol, cfg.deflation.power_maxit};
+  c.use_deflation = cfg.use_deflation ? 1 : 0;
+  c.continuation = cfg.continuation ? 1 : 0;
+  c.continuation_steps = cfg.continuation_steps;
+  pgm_newton_report r{};
+  detail::check(pgm_newton_solve(ctx, n_e, lambda, u.data(), 0, &c, &r), ctx);
+  NewtonReport out;
+  for (std::uint32_t i = 0; i < r.n_iters; ++i)
+    out.iters.push_back({r.iters[i].iter, r.iters[i].lambda, r.iters[i].update_inf,
+                         r.iters[i].residual_norm, r.iters[i].gmres_restarts,
+                         r.iters[i].gmres_inner});
+  out.converged = r.converged != 0;
+  out.final_residual = r.final_residual;
+  out.final_update = r.final_update;
+  out.total_inner = r.total_inner;
+  out.seconds = r.seconds;
+  pgm_newton_report_free(&r);
+  return out;
+}
+
 }  // namespace pgmres
+

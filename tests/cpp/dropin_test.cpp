@@ -1,3 +1,4 @@
+#include <algorithm>
 // C++ drop-in check: the reference's call sequence (newton.cpp:53-63 for the
 // first Newton system) written against include/pgmres/dgmres.hpp.  Prints one
 // line "restarts total_inner rank final_relative mu x_norm" for the pytest
@@ -66,5 +67,18 @@ int main(int argc, char** argv) {
   } catch (const std::runtime_error& e) {
     threw = std::string(e.what()).find("gmres: ") == 0;
   }
-  return threw ? 0 : 5;
+  if (!threw) return 5;
+  // newton_solve (newton.hpp:53-54) on the n_e = 8 system: the reference converges
+  // in 8 iterations to max u = 1.323002464567 (test_output.txt, criterion 7)
+  {
+    pgmres::DeviceExecutor exn(0);
+    pgmres::DenseVector u;
+    auto nr = pgmres::newton_solve(8, 6.8, u, pgmres::NewtonConfig{}, exn);
+    double umax = 0.0;
+    for (double v : u) umax = std::max(umax, v);
+    std::fprintf(stderr, "newton %zu iterations, max u %.12f\n", nr.iters.size(), umax);
+    if (!nr.converged || nr.iters.size() != 8 || std::fabs(umax - 1.323002464567) > 1e-11)
+      return 6;
+  }
+  return 0;
 }

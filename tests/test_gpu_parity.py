@@ -70,6 +70,31 @@ def test_spmv_bitexact_irregular(torch_cuda, ref):
     assert np.array_equal(ex.spmv(A, x), ref.spmv(Csr(n, rp, ci, va), x))
 
 
+def test_spmv_bitexact_wide_gaps_32bit_columns(torch_cuda, ref):
+    """Column gaps >= 65536 force the 32-bit column layout (the 16-bit delta
+    layout is used otherwise); both must give the reference's bits."""
+    rng = np.random.default_rng(11)
+    n = 70000
+    lens = rng.integers(1, 6, n)
+    rp = np.zeros(n + 1, np.uint32)
+    rp[1:] = np.cumsum(lens)
+    cols = []
+    for i, l in enumerate(lens):
+        c = {i, 0, n - 1} if i % 97 == 0 else {i}
+        while len(c) < max(l, len(c)):
+            c.add(int(rng.integers(0, n)))
+        cols.append(np.array(sorted(c), np.uint32))
+    lens = np.array([len(c) for c in cols])
+    rp[1:] = np.cumsum(lens)
+    ci = np.concatenate(cols).astype(np.uint32)
+    va = rng.standard_normal(rp[-1])
+    A = pg.CsrMatrix(n, rp, ci, va)
+    x = rng.standard_normal(n)
+    ex = pg.DeviceExecutor()
+    from oracle.refbind import Csr
+    assert np.array_equal(ex.spmv(A, x), ref.spmv(Csr(n, rp, ci, va), x))
+
+
 def test_spmv_device_pointers(torch_cuda, ref):
     torch = torch_cuda
     A, Ar, _ = _csr(ref, 4)
