@@ -56,7 +56,11 @@ __device__ __forceinline__ void spmv_tile(const Sell& A, const double* __restric
   constexpr int UG = SPMV_UNROLL / 4;  // 4-entry groups in flight per lane
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
-  for (int sl = warp; sl < SPT; sl += nw) {
+  // Rows are sorted by length inside the tile, so slice lengths fall with the
+  // slice index: warp w takes slices w and SPT-1-w (long + short), which
+  // balances the warps ahead of the epilogue barrier.
+  for (int it = 0; it < SPT / nw; ++it) {
+    const int sl = (it & 1) ? (SPT - 1 - (it >> 1) * nw - warp) : ((it >> 1) * nw + warp);
     const size_t s = (size_t)tile * SPT + sl;
     const unsigned long long base = A.sptr[s];
     const int L4 = (int)((A.sptr[s + 1] - base) >> 7);
@@ -348,6 +352,9 @@ __device__ __forceinline__ const double* epi_input(const Params& P, const PushEp
 constexpr int EPI_SMALL = 8 + 64;  // prologue scratch (doubles)
 constexpr int SPMV_WARPS = SPMV_THREADS / 32;
 
+__host__ __device__ constexpr size_t spmv_step_smem_doubles(int nv) {
+  return (size_t)EPI_SMALL + TILE + 2 * (size_t)nv + 2;
+}
 __host__ __device__ constexpr size_t spmv_smem_doubles(int nv) {
   return (size_t)EPI_SMALL + TILE + (size_t)SPMV_WARPS * TP_DOUBLES +
          (size_t)SPMV_WARPS * NVL * TPR + 2 * (size_t)nv + 2;
@@ -395,9 +402,11 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
   const int nv = E.nvals(P);
   double* small = sm;
   double* ys = sm + EPI_SMALL;
+  // the step epilogue needs no transpose tiles: [small | ys | bvals | red]
+  constexpr bool STEP = std::is_same<Epi, StepEpi>::value;
   double* tp = ys + TILE + (threadIdx.x >> 5) * TP_DOUBLES;
   double* wacc = ys + TILE + SPMV_WARPS * TP_DOUBLES;
-  double* bvals = wacc + SPMV_WARPS * NVL * TPR;
+  double* bvals = STEP ? ys + TILE : wacc + SPMV_WARPS * NVL * TPR;
   double* red = bvals + nv;
   E.prologue(P, small);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

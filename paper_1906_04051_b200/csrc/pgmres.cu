@@ -338,7 +338,9 @@ Status launch_spmv_k(pgm_context* ctx, int G, size_t smem, const Sell& sv, const
 template <class Epi>
 Status launch_spmv(pgm_context* ctx, const pgm_matrix* A, const Params& P, const Epi& E,
                    int nvmax, uint32_t prof_k = 0, int seg = 0) {
-  const size_t smem = spmv_smem(nvmax);
+  const size_t smem = std::is_same<Epi, StepEpi>::value
+                          ? sizeof(double) * spmv_step_smem_doubles(nvmax)
+                          : spmv_smem(nvmax);
   Sell sv = A->view();
   SpmvSeg sg{0, 0, 0};
   int G = std::max(1, A->ntiles);
