@@ -1113,43 +1113,57 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
     return;
   }
   const double tol = d->inv_tol;
-  // ---- largest_ritz_value: power iteration (deflation.cpp:57-82)
+  // ---- largest_ritz_value: power iteration (deflation.cpp:57-82).  Block
+  // sums with one barrier each (rotating slot arrays), the H z buffer swaps
+  // roles with the iterate instead of being copied: 5 barriers per iteration.
+  __shared__ double sA[RITZ_THREADS / 32], sB[RITZ_THREADS / 32], sC[RITZ_THREADS / 32];
+  auto bsum1 = [&](double v, double* slots) {
+    v = warp_sum(v);
+    if ((tid & 31) == 0) slots[tid >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += slots[w];
+    return t;
+  };
   {
+    double* it_x = nx;  // H z of the current iterate
+    double* it_h = hz;
     for (int i = tid; i < k; i += blockDim.x) z[i] = 1.0 / sqrt((double)k);
     __syncthreads();
-    hmatvec(H, k, z, nx);
+    hmatvec(H, k, z, it_x);
     __syncthreads();
     bool have = false, conv = false, broke = false;
     double val = 0.0;
     for (int it = 0; it < d->pow_maxit; ++it) {
       double p = 0.0;
-      for (int i = tid; i < k; i += blockDim.x) p += nx[i] * nx[i];
-      const double nz = sqrt(block_sum(p, s_red));
+      for (int i = tid; i < k; i += blockDim.x) p += it_x[i] * it_x[i];
+      const double nz = sqrt(bsum1(p, sA));
       if (!isfinite(nz) || nz == 0.0) {
         broke = true;
         break;
       }
-      for (int i = tid; i < k; i += blockDim.x) z[i] = nx[i] / nz;
+      for (int i = tid; i < k; i += blockDim.x) z[i] = it_x[i] / nz;
       __syncthreads();
-      hmatvec(H, k, z, hz);
+      hmatvec(H, k, z, it_h);
       __syncthreads();
       double q = 0.0;
-      for (int i = tid; i < k; i += blockDim.x) q += z[i] * hz[i];
-      const double theta = block_sum(q, s_red);
+      for (int i = tid; i < k; i += blockDim.x) q += z[i] * it_h[i];
+      const double theta = bsum1(q, sB);
       double e = 0.0;
       for (int i = tid; i < k; i += blockDim.x) {
-        const double t = hz[i] - theta * z[i];
+        const double t = it_h[i] - theta * z[i];
         e += t * t;
       }
-      const double resid = sqrt(block_sum(e, s_red));
+      const double resid = sqrt(bsum1(e, sC));
       val = theta;
       have = true;
       if (resid <= tol * scale) {
         conv = true;
         break;
       }
-      for (int i = tid; i < k; i += blockDim.x) nx[i] = hz[i];  // H z of the new z
-      __syncthreads();
+      double* t = it_x;  // H z of the new z
+      it_x = it_h;
+      it_h = t;
     }
     const bool ok = conv || (!broke && have);
     if (tid == 0 && ok && isfinite(val) && fabs(val) > fabs(d->mu)) d->mu = val;  // observe_ritz
@@ -1211,7 +1225,7 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
   }
   load_h();  // H again for theta / residuals
   __syncthreads();
-  // ---- smallest_ritz_pair: inverse power iteration (deflation.cpp:31-54)
+  // ---- smallest_ritz_pair: inverse power iteration (deflation.cpp:31-54), 6 barriers / it
   for (int i = tid; i < k; i += blockDim.x) z[i] = 1.0 / sqrt((double)k);
   __syncthreads();
   bool conv = false;
@@ -1221,7 +1235,7 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
     __syncthreads();
     double p = 0.0;
     for (int i = tid; i < k; i += blockDim.x) p += nx[i] * nx[i];
-    const double nz = sqrt(block_sum(p, s_red));
+    const double nz = sqrt(bsum1(p, sA));
     if (!isfinite(nz) || nz == 0.0) break;
     for (int i = tid; i < k; i += blockDim.x) z[i] = nx[i] / nz;
     __syncthreads();
@@ -1229,13 +1243,13 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
     __syncthreads();
     double q = 0.0;
     for (int i = tid; i < k; i += blockDim.x) q += z[i] * hz[i];
-    const double theta = block_sum(q, s_red);
+    const double theta = bsum1(q, sB);
     double e = 0.0;
     for (int i = tid; i < k; i += blockDim.x) {
       const double t = hz[i] - theta * z[i];
       e += t * t;
     }
-    const double resid = sqrt(block_sum(e, s_red));
+    const double resid = sqrt(bsum1(e, sC));
     val = theta;
     if (resid <= tol * scale) {
       conv = true;
