@@ -8,7 +8,10 @@
 namespace pgm {
 
 // ---- launch geometry -------------------------------------------------------
-constexpr int TILE = 512;             // rows per SpMV tile (SELL sort window)
+#ifndef PGM_TILE
+#define PGM_TILE 512
+#endif
+constexpr int TILE = PGM_TILE;        // rows per SpMV tile (SELL sort window)
 constexpr int SPT = TILE / 32;        // 32-row slices per tile
 constexpr int SPMV_THREADS = 256;
 #ifndef PGM_SPMV_UNROLL

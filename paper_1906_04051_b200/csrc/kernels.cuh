@@ -1350,15 +1350,16 @@ __global__ void __launch_bounds__(256) k_sell_layout(const unsigned* rp, int n,
                                                      unsigned long long nnz, unsigned* lane_len,
                                                      unsigned short* lane_row,
                                                      unsigned long long* sptr, int* bad) {
-  using Sort = cub::BlockRadixSort<unsigned, 256, 2, int>;
+  constexpr int IPT = TILE / 256;  // rows per thread
+  using Sort = cub::BlockRadixSort<unsigned, 256, IPT, int>;
   __shared__ typename Sort::TempStorage tmp;
   __shared__ unsigned s_len[TILE];
   const int tile = blockIdx.x;
   const int r0 = tile * TILE;
-  unsigned key[2];
-  int val[2];
-  for (int q = 0; q < 2; ++q) {
-    const int i = threadIdx.x * 2 + q;  // blocked arrangement: keeps the original order
+  unsigned key[IPT];
+  int val[IPT];
+  for (int q = 0; q < IPT; ++q) {
+    const int i = threadIdx.x * IPT + q;  // blocked arrangement: keeps the original order
     const int row = r0 + i;
     unsigned len = 0;
     if (row < n) {
@@ -1373,8 +1374,8 @@ __global__ void __launch_bounds__(256) k_sell_layout(const unsigned* rp, int n,
   if (tile == 0 && threadIdx.x == 0 && (rp[0] != 0u || (unsigned long long)rp[n] != nnz))
     atomicOr(bad, 1);
   Sort(tmp).SortDescending(key, val);
-  for (int q = 0; q < 2; ++q) {
-    const int j = threadIdx.x * 2 + q;  // sorted position = slice * 32 + lane
+  for (int q = 0; q < IPT; ++q) {
+    const int j = threadIdx.x * IPT + q;  // sorted position = slice * 32 + lane
     const int row = r0 + val[q];
     const bool real = key[q] != 0u;
     const unsigned len = real ? key[q] - 1u : 0u;

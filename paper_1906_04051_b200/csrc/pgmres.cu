@@ -450,7 +450,11 @@ Status launch_cgs2_r(pgm_context* ctx, const Params& P, int k, int rev, int npw,
 Status launch_cgs2_b(pgm_context* ctx, const Params& P, int k, int nv, int rev, int r) {
   constexpr int R = PGM_CGS2_RPL;
   const int np = k + 1;
-  if (np <= 64) return launch_cgs2_r<4, R, 16>(ctx, P, k, rev, (np + 3) / 4, r);
+#ifndef PGM_B_NW
+#define PGM_B_NW 4
+#endif
+  constexpr int BNW = PGM_B_NW;
+  if (np <= 64) return launch_cgs2_r<BNW, R, (64 + BNW - 1) / BNW>(ctx, P, k, rev, (np + BNW - 1) / BNW, r);
   if (np <= CGS2_SPLIT_MAX) return launch_cgs2_r<8, R, 14>(ctx, P, k, rev, (np + 7) / 8, r);
   return launch_sweep_np<SW_CGS2_B, 0>(ctx, P, k, nv, np);
 }
