@@ -6,8 +6,10 @@
 One step = one complete deflated_gmres solve of the first Newton system
 J(0) x = -R(0) of the 3-D Bratu FEM problem (lambda = 6.8, x0 = 0),
 GMRES(50) + deflation (r_max = 20), rel_tol = 1e-10.  Default workload is
-BASELINE config 2: n_e = 50, 1,030,301 DOF, 62,606,425 nnz (the matrix,
-751 MB, is larger than the 126 MB L2, so no L2 flush is needed).
+BASELINE config 3, the largest benchmark mesh, quoted "at 1/2/4/8 B200":
+n_e = 125, 15,813,251 DOF, 991,266,025 nnz (the matrix, 11.9 GB, dwarfs the
+126 MB L2, so no L2 flush is needed); --gpus N row-block partitions it
+(strong scaling).  --ne 50 is BASELINE config 2 (1,030,301 DOF).
 
 `value`  : GMRES iterations/s with inputs resident in HBM (CUDA events on the
            library stream, max over ranks).
@@ -17,7 +19,8 @@ BASELINE config 2: n_e = 50, 1,030,301 DOF, 62,606,425 nnz (the matrix,
            the CGS2 pass-1 dots), algorithmic bytes / its CUDA-event duration.
 `cpu_baseline`: the reference CPU solver (oracle/_ref, the reference's own
            sources) on a bounded sample of the same system, all host cores.
---impl reference: the reference CPU solver itself, rank 0 only.
+--impl reference: the reference CPU solver itself, rank 0 only (a bounded
+           sample per step: one fixed restart cycle on n_e > 50).
 """
 from __future__ import annotations
 
@@ -36,6 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 LAMBDA = 6.8
+_OUT = sys.stdout
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 
 
@@ -45,11 +49,16 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="pgmres", choices=["pgmres", "reference"])
-    ap.add_argument("--ne", type=int, default=50)
+    ap.add_argument("--ne", type=int, default=125,
+                    help="mesh: n_e = 125 is BASELINE config 3 (the largest benchmark mesh, "
+                         "15.8 M DOF, quoted at 1/2/4/8 B200); n_e = 50 is config 2")
     ap.add_argument("--m", type=int, default=50)
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--nccl-selftest", action="store_true",
+                    help="N=1 in collective mode (1-rank NCCL communicator): every reduction "
+                         "pays an ncclAllReduce + k_finish, as on each rank of an N-GPU run")
     return ap.parse_args()
 
 
@@ -59,7 +68,9 @@ def metric_name(a):
 
 
 def workload(a, n, nnz):
-    return {"workload": f"cfg2-equivalent: 3-D Bratu first Newton system, n_e={a.ne} "
+    tag = {125: "BASELINE config 3 (4000x4000-equivalent, largest benchmark mesh)",
+           50: "BASELINE config 2 (1000x1000-equivalent)"}.get(a.ne, "custom mesh")
+    return {"workload": f"{tag}: 3-D Bratu first Newton system, n_e={a.ne} "
                         f"({n:,} DOF, {nnz:,} nnz), GMRES({a.m}) + deflation r_max=20, "
                         f"rel_tol={a.tol:g}, x0=0",
             "n_e": a.ne, "dof": n, "nnz": nnz, "m": a.m, "rel_tol": a.tol, "r_max": 20,
@@ -182,6 +193,10 @@ def run_gpu(a):
             idt.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().numpy())
+    elif a.nccl_selftest:
+        from paper_1906_04051_b200.dgmres import nccl_unique_id
+
+        nccl_id = nccl_unique_id()
     ex = pg.DeviceExecutor(local, n_global=na ** 3, n_axis=na if world > 1 else 0, rank=rank,
                            world=world, nccl_id=nccl_id)
     A_d, b_d = ex.assemble_bratu(a.ne, LAMBDA, device=True)
@@ -267,9 +282,10 @@ def run_gpu(a):
     achieved = sp[0] / sp[1] / 1e9
     traffic = None  # measured DRAM bytes per launch of this kernel (ncu, profiles/)
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp) and a.ne == 50 and a.m == 50 and world == 1:
+    if os.path.exists(tp) and a.m == 50 and world == 1:
         with open(tp) as f:
-            traffic = json.load(f).get("k_spmv<StepEpi>", {}).get("dram_bytes_per_launch")
+            traffic = json.load(f).get(f"n_e={a.ne}", {}).get("k_spmv<StepEpi>", {}).get(
+                "dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "frac_dram": (round(traffic / (sp[1] / max(1, sp[2])) / 1e9 / peak, 4)
@@ -356,7 +372,7 @@ def run_gpu(a):
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(a)
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        print(json.dumps(out), file=_OUT, flush=True)
     if dist:
         dist.destroy_process_group()
 
@@ -374,10 +390,11 @@ def cpu_baseline(a):
     na = 2 * a.ne + 1
     th = _ref_threads(na)
     A, b = R.first_newton_system(a.ne, LAMBDA, threads=th)
-    r = R.solve(A, b, m=a.m, max_restarts=2, fixed_iterations=True, ne=a.ne, threads=th)
+    cycles = 2 if a.ne <= 50 else 1  # ~2-40 s of CPU work
+    r = R.solve(A, b, m=a.m, max_restarts=cycles, fixed_iterations=True, ne=a.ne, threads=th)
     return {"value": round(r.total_inner / r.wall_s, 3), "unit": "iter/s", "cores": th,
             "kind": "reference",
-            "sample": f"2 fixed restart cycles ({r.total_inner} inner iterations) of deflated "
+            "sample": f"{cycles} fixed restart cycle(s) ({r.total_inner} inner iterations) of deflated "
                       f"GMRES({a.m}) on the same n_e={a.ne} system, deterministic executor, "
                       f"{th} threads, {r.wall_s:.2f} s",
             "cpu_model": _cpu_model()}
@@ -404,13 +421,16 @@ def run_reference(a):
     th = _ref_threads(na)
     A, b = R.first_newton_system(a.ne, LAMBDA, threads=th)
     kw = dict(m=a.m, ne=a.ne, threads=th)
-    full = R.solve(A, b, max_restarts=100, rel_tol=a.tol, **kw)  # warm-up 0: full solve
-    if full.wall_s <= 20.0:
+    # bounded sample: one fixed restart cycle (m inner iterations) per step; the
+    # full tolerance solve per step only where it takes seconds (n_e <= 50)
+    if a.ne <= 50:
+        full = R.solve(A, b, max_restarts=100, rel_tol=a.tol, **kw)  # warm-up 0
         sample = dict(max_restarts=100, rel_tol=a.tol)
         desc = f"full tolerance solve ({full.total_inner} inner iterations)"
     else:
         sample = dict(max_restarts=1, fixed_iterations=True)
         desc = f"1 fixed restart cycle ({a.m} inner iterations)"
+        R.solve(A, b, **sample, **kw)  # warm-up 0
     for _ in range(max(0, a.warmup - 1)):
         R.solve(A, b, **sample, **kw)
     iters, secs = 0, 0.0
@@ -431,10 +451,16 @@ def run_reference(a):
                             "cpu_model": _cpu_model()},
            "e2e": {"value": round(v, 3), "unit": "iter/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    print(json.dumps(out), file=_OUT, flush=True)
 
 
 def main():
+    # exactly one JSON line on stdout: libraries (NCCL's version banner, ...)
+    # print to fd 1, so fd 1 points at stderr until the result is printed
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    global _OUT
+    _OUT = os.fdopen(saved, "w")
     a = parse()
     if a.impl == "reference":
         run_reference(a)

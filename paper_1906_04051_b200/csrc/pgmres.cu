@@ -129,6 +129,10 @@ struct pgm_loopback {
 
 struct pgm_context {
   int device = 0, rank = 0, world = 1;
+  // collective mode: reductions go through red_out + allreduce + k_finish.
+  // world > 1, or a 1-rank NCCL communicator (world = 1 with an nccl_id:
+  // exercises the NCCL path on one GPU).
+  bool coll = false;
   uint32_t n_axis = 0, n_global = 0;
   pgm_partition part{};
   size_t n = 0, lo = 0, hi = 0, ld = 0;
@@ -641,7 +645,7 @@ Params make_params(pgm_context* ctx, pgm_deflator* d) {
   P.gpart = ctx->gpart_buf;
   P.cnt = ctx->cnt;
   P.red_out = ctx->red_out;
-  P.world = ctx->world;
+  P.world = ctx->coll ? std::max(ctx->world, 2) : 1;
   return P;
 }
 
@@ -668,7 +672,7 @@ Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot = 0, cudaStream_t
 
 template <int KIND>
 Status finish_global(pgm_context* ctx, const Params& P, int k, int nv) {
-  if (ctx->world == 1) return {};
+  if (!ctx->coll) return {};
   if (nv <= 0 || nv > ctx->nvmax) return Status{PGM_ESTATE, "finish_global: bad reduction size"};
   TRY(allreduce_red(ctx, nv));
   k_finish<KIND><<<1, 32, 0, ctx->stream>>>(P, k);
@@ -1217,12 +1221,13 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) 
     ctx->loop = L;
     std::lock_guard<std::mutex> lk(L->mu);
     L->ctx[cfg->rank] = ctx;
-  } else if (cfg->world > 1) {
+  } else if (cfg->world > 1 || cfg->nccl_id) {
     if (!nccl_lite::available()) return bail(Status{PGM_ENCCL, "libnccl.so.2 not loadable"});
     if (!cfg->nccl_id) return bail(Status{PGM_EINVAL, "world > 1 needs an ncclUniqueId"});
     if (nccl_lite::comm_init_rank(&ctx->nccl, cfg->world, cfg->nccl_id, cfg->rank) != 0)
       return bail(Status{PGM_ENCCL, "ncclCommInitRank failed"});
   }
+  ctx->coll = ctx->world > 1 || ctx->nccl != nullptr;
   // dummy deflator (r = 0 forever) for plain gmres_restarted solves
   pgm_deflation_config dc{1, 1, 1e-8, 1, 1e-10, 1};
   pgm_deflator* dd = nullptr;
@@ -1809,7 +1814,7 @@ Status newton_scalars(pgm_context* ctx, const double* rhs_own, const double* del
   k_newton_final<<<1, 256, 0, ctx->stream>>>(ctx->part_buf, G, ctx->red_out, nv, ctx->rank);
   ctx->launches += 2;
   CU(cudaGetLastError());
-  if (ctx->world > 1) TRY(allreduce_red(ctx, nv));
+  if (ctx->coll) TRY(allreduce_red(ctx, nv));
   double h[1 + 64];
   CU(cudaMemcpyAsync(h, ctx->red_out, 8 * (size_t)nv, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));

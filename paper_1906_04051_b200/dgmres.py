@@ -194,6 +194,9 @@ class DeviceExecutor:
         if self.world > 1 and self._loop is None:
             if self._nccl_id is None or len(self._nccl_id) != 128:
                 raise ValueError("world > 1 needs a 128-byte ncclUniqueId or a LoopbackGroup")
+        if self._nccl_id is not None and self._loop is None:
+            # world = 1 with an id: a 1-rank NCCL communicator (collective mode
+            # on one GPU: every reduction goes through ncclAllReduce + k_finish)
             idbuf = C.create_string_buffer(bytes(self._nccl_id), 128)
         cfg = capi.ContextConfig(self.device, self.rank, self.world,
                                  C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
