@@ -448,6 +448,9 @@ Status launch_cgs2_r(pgm_context* ctx, const Params& P, int k, int rev, int npw,
   if (nuw <= 1) return launch_cgs2_nuw<NW, R, 1, NPWMAX>(ctx, P, k, rev, npw);
   if (nuw <= 2) return launch_cgs2_nuw<NW, R, 2, NPWMAX>(ctx, P, k, rev, npw);
   if (nuw <= 4) return launch_cgs2_nuw<NW, R, 4, NPWMAX>(ctx, P, k, rev, npw);
+  if constexpr (NW == 4) {
+    if (nuw <= 6) return launch_cgs2_nuw<NW, R, 6, NPWMAX>(ctx, P, k, rev, npw);
+  }
   return launch_cgs2_nuw<NW, R, (MAX_R1 + NW - 1) / NW, NPWMAX>(ctx, P, k, rev, npw);
 }
 

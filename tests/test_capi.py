@@ -55,3 +55,23 @@ def test_partition_rejects_bad_worker_counts(lib):
     assert _part(lib, 5, 0, 0)[0] == _capi.PGM_EINVAL
     assert _part(lib, 5, 6, 0)[0] == _capi.PGM_EINVAL
     assert _part(lib, 5, 5, 4)[0] == 0
+
+
+def test_newton_config_and_report_mirror_reference():
+    """NewtonConfig defaults (newton.hpp:15-23), ctypes layout of the C struct,
+    and NewtonReport::write_csv (newton.cpp:12-19: header, precision 17)."""
+    import paper_1906_04051_b200 as pg
+
+    c = pg.NewtonConfig()
+    assert (c.max_iters, c.update_tol, c.use_deflation, c.continuation,
+            c.continuation_steps) == (30, 1e-8, True, False, 4)
+    assert (c.gmres.m, c.gmres.max_restarts, c.gmres.rel_tol) == (50, 100, 1e-10)
+    cc = c._c()
+    assert cc.max_iters == 30 and cc.gmres.m == 50 and cc.deflation.r_max == 20
+    assert C.sizeof(_capi.NewtonRecordC) == 48
+    rep = pg.NewtonReport([pg.NewtonIterRecord(1, 6.8, 0.7895591656135857, 0.12056974500368113,
+                                               2, 66)], True)
+    assert rep.write_csv() == ("iter,update_inf_norm,residual_2norm,gmres_restarts\n"
+                               "1,0.78955916561358575,0.12056974500368113,2\n")
+    with pytest.raises(ValueError):
+        pg.NewtonConfig(max_iters=-1)._c()
