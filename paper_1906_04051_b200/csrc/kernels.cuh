@@ -377,6 +377,10 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
   const int tile = SEG ? ((int)blockIdx.x < sg.len0 ? sg.b0 + (int)blockIdx.x
                                                     : sg.b1 + ((int)blockIdx.x - sg.len0))
                        : (int)blockIdx.x;
+  // A step SpMV of a cycle that already stopped exits before touching the
+  // matrix: g->active is written by pass B's finisher, >= 2 kernels back
+  // (common.cuh PDL rule), so it is final here.
+  if (std::is_same<Epi, StepEpi>::value && !*(volatile const int*)&P.g->active) return;
 #if PGM_SPMV_PREFETCH && PGM_SPMV_EARLY_PF
   {
     // L2 prefetch of this warp's first slice (values + column ids).  The

@@ -166,6 +166,7 @@ struct pgm_context {
   struct pgm_loopback* loop = nullptr;
   pgm_deflator* cur_defl = nullptr;  // deflator of the running solve (halo of u)
   double* halo_ptr = nullptr;        // HV_PTR: ctx-layout view of a caller vector (Newton u)
+  std::vector<pgm_matrix*> mats;     // live matrices (detached when the context dies first)
   // optional per-launch profiling (CUDA events around every hot-path kernel)
   bool prof_on = false;
   bool pdl = true;  // programmatic dependent launch of the hot-path kernels (PGMRES_PDL=0 disables)
@@ -1012,6 +1013,7 @@ Status matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags, pgm
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess)
     return cleanup(Status{PGM_ECUDA, std::string("csr->sell: ") + cudaGetErrorString(e)});
+  ctx->mats.push_back(M);
   *out = M;
   return {};
 }
@@ -1250,6 +1252,8 @@ void pgm_context_destroy(pgm_context* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (pgm_matrix* m : ctx->mats) m->ctx = nullptr;  // destroyed later with plain frees
+  ctx->mats.clear();
   if (ctx->dummy) pgm_deflator_destroy(ctx->dummy);
   free_workspace(ctx);
   dfree(ctx->x);
@@ -1304,6 +1308,10 @@ pgm_status pgm_matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t fl
 
 pgm_status pgm_matrix_update_values(pgm_matrix* a, const double* values, int32_t flags) {
   if (!a) return PGM_EINVAL;
+  if (!a->ctx) {
+    g_tls_err = "pgm_matrix_update_values: the matrix's context was destroyed";
+    return PGM_ESTATE;
+  }
   pgm_context* ctx = a->ctx;
   cudaStream_t st = ctx->stream;
   cudaError_t e = cudaMemcpyAsync(a->vstage, values, 8 * a->nnz,
@@ -1323,19 +1331,34 @@ pgm_status pgm_matrix_update_values(pgm_matrix* a, const double* values, int32_t
 
 void pgm_matrix_destroy(pgm_matrix* a) {
   if (!a) return;
-  cudaStream_t st = a->ctx ? a->ctx->stream : nullptr;
-  dfree_async(a->sptr, st);
-  dfree_async(a->lane_len, st);
-  dfree_async(a->lane_row, st);
-  dfree_async(a->val, st);
-  dfree_async(a->col, st);
-  dfree_async(a->col16, st);
-  dfree_async(a->lane_base, st);
-  dfree_async(a->rp, st);
-  dfree_async(a->vstage, st);
+  pgm_context* ctx = a->ctx;
+  if (ctx) {
+    auto& v = ctx->mats;
+    v.erase(std::remove(v.begin(), v.end(), a), v.end());
+    cudaStream_t st = ctx->stream;
+    dfree_async(a->sptr, st);
+    dfree_async(a->lane_len, st);
+    dfree_async(a->lane_row, st);
+    dfree_async(a->val, st);
+    dfree_async(a->col, st);
+    dfree_async(a->col16, st);
+    dfree_async(a->lane_base, st);
+    dfree_async(a->rp, st);
+    dfree_async(a->vstage, st);
+  } else {  // its context was destroyed first: plain (synchronous) frees
+    cudaDeviceSynchronize();
+    dfree(a->sptr);
+    dfree(a->lane_len);
+    dfree(a->lane_row);
+    dfree(a->val);
+    dfree(a->col);
+    dfree(a->col16);
+    dfree(a->lane_base);
+    dfree(a->rp);
+    dfree(a->vstage);
+  }
   delete a;
 }
-
 pgm_status pgm_matrix_info(const pgm_matrix* a, uint32_t* n, uint64_t* nnz, uint64_t* stored,
                            uint64_t* device_bytes) {
   if (!a) return PGM_EINVAL;
@@ -1349,6 +1372,10 @@ pgm_status pgm_matrix_info(const pgm_matrix* a, uint32_t* n, uint64_t* nnz, uint
 }
 
 pgm_status pgm_spmv(pgm_matrix* a, const double* x, double* y, int32_t flags) {
+  if (a && !a->ctx) {
+    g_tls_err = "pgm_spmv: the matrix's context was destroyed";
+    return PGM_ESTATE;
+  }
   if (!a) return PGM_EINVAL;
   pgm_context* ctx = a->ctx;
   cudaSetDevice(ctx->device);
