@@ -477,6 +477,63 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
     if (grid_reduce_ex(bvals, nv, P, red, G, tile)) E.finish(P, red);
     return;
   }
+  if constexpr (std::is_same<Epi, PushEpi>::value) {
+    // push_vector tail (deflation.cpp:160-174), same two-phase scheme as the
+    // step epilogue: (1) U_j = u ps, AU_j = (A u) ps per row into smem;
+    // (2) the 2j+1 T row/column dots, warp-split over the vector families
+    // U_l . AU_j (l < j), U_j . AU_j, U_j . AU_l (l < j).
+    const int j = P.d->r;
+    const size_t ld = P.ld;
+    const int row0 = tile * TILE;
+    const int rows = min(TILE, A.n - row0);
+    const double ps = small[0];
+    double* an = ys;      // (A u) ps, in place
+    double* un = tp - (threadIdx.x >> 5) * TP_DOUBLES;  // the transpose area: TILE doubles
+    for (int i = threadIdx.x; i < TILE; i += SPMV_THREADS) {
+      double a = 0.0, uu = 0.0;
+      if (i < rows) {
+        uu = P.u[P.lo + row0 + i] * ps;
+        a = ys[i] * ps;
+        P.U[(size_t)j * ld + P.lo + row0 + i] = uu;
+        P.AU[(size_t)j * ld + P.lo + row0 + i] = a;
+      }
+      an[i] = a;
+      un[i] = uu;
+    }
+    __syncthreads();
+    for (int v = warp; v < nv; v += SPMV_WARPS) {
+      double a[4] = {0.0, 0.0, 0.0, 0.0};
+      if (v == j) {
+        for (int q = 0; q < TILE / 32; ++q) a[q & 3] += un[lane + 32 * q] * an[lane + 32 * q];
+      } else {
+        const double* vec = (v < j ? P.U + (size_t)v * ld : P.AU + (size_t)(v - j - 1) * ld) +
+                            P.lo + row0 + lane;
+        const double* mul = v < j ? an : un;
+        if (rows == TILE) {
+          double t[TILE / 32];
+#pragma unroll
+          for (int q = 0; q < TILE / 32; ++q) t[q] = __ldg(vec + 32 * q);
+#pragma unroll
+          for (int q = 0; q < TILE / 32; ++q) a[q & 3] += t[q] * mul[lane + 32 * q];
+        } else {
+          for (int q = 0; q < TILE / 32; ++q)
+            if (lane + 32 * q < rows) a[q & 3] += __ldg(vec + 32 * q) * mul[lane + 32 * q];
+        }
+      }
+      const double sum = warp_sum((a[0] + a[1]) + (a[2] + a[3]));
+      if (lane == 0) bvals[v] = sum;
+    }
+    pdl_trigger();
+    __syncthreads();
+    const int G = SEG ? A.ntiles : (int)gridDim.x;
+    if (P.world > 1) {
+      if (grid_reduce_ex(bvals, nv, P, red, G, tile))
+        for (int v = threadIdx.x; v < nv; v += blockDim.x) P.red_out[v] = red[v];
+      return;
+    }
+    if (grid_reduce_ex(bvals, nv, P, red, G, tile)) E.finish(P, red);
+    return;
+  }
   double acc[NVL];
 #pragma unroll
   for (int s = 0; s < NVL; ++s) acc[s] = 0.0;

@@ -471,10 +471,16 @@ Status launch_cgs2_b(pgm_context* ctx, const Params& P, int k, int nv, int rev, 
 // np picks the register-resident template (0 = generic path for np > 64).
 template <int MODE>
 Status launch_sweep(pgm_context* ctx, const Params& P, int k, int np, int /*np2*/, int nv, bool) {
+  // register-resident vector set up to NPMAX; above it the 16-wide generic
+  // loop (measured at cfg3: the push_vector sweeps are faster generic, the x
+  // update register-resident)
+  constexpr int NPMAX = MODE == SW_XUPDATE ? 64 : 16;
   if (np <= 8) return launch_sweep_np<MODE, 8>(ctx, P, k, nv, np);
   if (np <= 16) return launch_sweep_np<MODE, 16>(ctx, P, k, nv, np);
-  if (np <= 32) return launch_sweep_np<MODE, 32>(ctx, P, k, nv, np);
-  if (np <= 64) return launch_sweep_np<MODE, 64>(ctx, P, k, nv, np);
+  if constexpr (NPMAX >= 64) {
+    if (np <= 32) return launch_sweep_np<MODE, 32>(ctx, P, k, nv, np);
+    if (np <= 64) return launch_sweep_np<MODE, 64>(ctx, P, k, nv, np);
+  }
   return launch_sweep_np<MODE, 0>(ctx, P, k, nv, np);
 }
 
