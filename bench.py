@@ -36,6 +36,8 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+if os.environ.get("PGMRES_PEER") == "1":  # before CUDA starts (pgm_peer_import requires it)
+    os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 sys.path.insert(0, ROOT)
 
 LAMBDA = 6.8
@@ -199,6 +201,13 @@ def run_gpu(a):
         nccl_id = nccl_unique_id()
     ex = pg.DeviceExecutor(local, n_global=na ** 3, n_axis=na if world > 1 else 0, rank=rank,
                            world=world, nccl_id=nccl_id)
+    if dist and os.environ.get("PGMRES_PEER") == "1":
+        # fused peer-memory allreduce inside the reduction kernels (CUDA IPC
+        # windows over NVLink) instead of NCCL allreduce + k_finish
+        mine = torch.frombuffer(bytearray(ex.peer_export()), dtype=torch.uint8).cuda()
+        allh = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(allh, mine)
+        ex.peer_import([bytes(h.cpu().numpy()) for h in allh])
     A_d, b_d = ex.assemble_bratu(a.ne, LAMBDA, device=True)
     n = ex.n_own
     nnz_local = A_d.nnz

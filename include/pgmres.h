@@ -171,6 +171,16 @@ void pgm_report_free(pgm_report* rep);
  * broadcast it, e.g. with torch.distributed). */
 pgm_status pgm_nccl_unique_id(void* out128);
 
+/* Peer-memory transport (world > 1, one process per GPU): every reduction
+ * kernel all-reduces inside its last block by storing its sums into every
+ * rank's window over NVLink (CUDA IPC mapping) — no NCCL call, no extra
+ * kernel.  Export this rank's 128-byte window handle, gather all ranks'
+ * handles in rank order (e.g. torch.distributed.all_gather), import them.
+ * Without the import the context keeps the NCCL allreduce.  In-process
+ * loopback groups use the peer transport by default (PGMRES_PEER=0: off). */
+pgm_status pgm_peer_export(pgm_context* ctx, void* out128);
+pgm_status pgm_peer_import(pgm_context* ctx, const void* all /* world * 128 bytes */);
+
 /* Kernel launches of the last pgm_solve (evidence for the bench). */
 uint64_t pgm_context_launch_count(const pgm_context* ctx);
 /* Optional CUDA-event timing of every hot-path kernel of the next solves

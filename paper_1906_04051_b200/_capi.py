@@ -82,7 +82,8 @@ EXPORTS = [
     "pgm_deflator_observe_ritz", "pgm_deflator_apply", "pgm_solve", "pgm_report_free",
     "pgm_context_launch_count", "pgm_context_set_profiling", "pgm_context_profile",
     "pgm_bratu_nnz", "pgm_bratu_assemble", "pgm_nccl_unique_id", "pgm_loopback_create",
-    "pgm_loopback_destroy", "pgm_newton_solve", "pgm_newton_report_free",
+    "pgm_loopback_destroy", "pgm_newton_solve", "pgm_newton_report_free", "pgm_peer_export",
+    "pgm_peer_import",
 ]
 
 _lib = None
@@ -137,6 +138,8 @@ def lib():
         "pgm_newton_solve": ([vp, u32, dbl, vp, i32, C.POINTER(NewtonConfigC),
                               C.POINTER(NewtonReportC)], C.c_int),
         "pgm_newton_report_free": ([C.POINTER(NewtonReportC)], None),
+        "pgm_peer_export": ([vp, vp], C.c_int),
+        "pgm_peer_import": ([vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -93,7 +93,18 @@ struct Params {
   unsigned* cnt;
   double* red_out;  // world > 1: block-reduced local sums for the allreduce
   int world;
+  // fused peer-memory allreduce (world > 1, peer mode): every rank's comm
+  // window is mapped into every other rank (NVLink P2P / CUDA IPC, or plain
+  // pointers for in-process ranks)
+  int peer, rank;
+  double* const* peer_win;                  // [world] -> window [2][world][PEER_NV]
+  unsigned long long* const* peer_flag;     // [world] -> flags  [2][world]
+  const double* win_local;
+  const unsigned long long* flag_local;
+  unsigned long long* epoch;                // this rank's reduction counter
 };
+
+constexpr int PEER_NV = 2 * MAX_R1 + MAX_M + 8;  // values per reduction slot
 
 // ---- programmatic dependent launch (PDL) -------------------------------------
 // The hot-path kernels are launched with programmatic stream serialization:
@@ -221,6 +232,89 @@ __device__ __forceinline__ bool grid_reduce_ex(const double* bvals, int nv, cons
 __device__ __forceinline__ bool grid_reduce(const double* bvals, int nv, const Params& P,
                                             double* red) {
   return grid_reduce_ex(bvals, nv, P, red, (int)gridDim.x, (int)blockIdx.x);
+}
+
+// ---- fused cross-GPU allreduce over peer memory --------------------------------
+// Called by every thread of the reduction's last block with red[0..nv) = this
+// rank's sums.  The block pushes them into slot [parity][rank] of EVERY
+// rank's window with plain stores over NVLink, fences system-wide, raises its
+// epoch flag in every window, waits until all ranks' flags reach the epoch,
+// then sums the world slots in rank order: identical bits on every rank, no
+// extra kernel, no NCCL call.  Epochs are per-rank counters that advance
+// identically (every rank runs the same reduction sequence); two parities
+// suffice because a rank can only run ahead by one reduction.  The wait is
+// bounded: on timeout the block gives up and flags g->error.
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __noinline__ void peer_allreduce(double* red, int nv, const Params& P) {
+  __shared__ unsigned long long s_e;
+  __shared__ int s_timeout;
+  const int W = P.world, me = P.rank;
+  if (threadIdx.x == 0) {
+    s_e = ++(*P.epoch);
+    s_timeout = 0;
+  }
+  __syncthreads();
+  const unsigned long long e = s_e;
+  const int par = (int)(e & 1ull);
+#ifdef PGM_PEER_DEBUG
+  if (threadIdx.x == 0 && e < 12) printf("peer rank %d e %llu nv %d grid %d\n", me, e, nv, (int)gridDim.x);
+#endif
+  for (int q = 0; q < W; ++q) {
+    double* dst = P.peer_win[q] + ((size_t)par * W + me) * PEER_NV;
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) dst[v] = red[v];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < W) st_release_sys(P.peer_flag[threadIdx.x] + par * W + me, e);
+  if (threadIdx.x < W) {
+    const unsigned long long* f = P.flag_local + par * W + threadIdx.x;
+    long long spins = 0;
+    while (ld_acquire_sys(f) < e) {
+      if (++spins > (1ll << 24)) {  // ~10 s
+        s_timeout = 1;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+#ifdef PGM_PEER_DEBUG
+  if (s_timeout && threadIdx.x == 0) printf("peer TIMEOUT rank %d e %llu\n", me, e);
+  if (threadIdx.x < W && e < 12) printf("peer rank %d sees flag[%d] = %llu\n", me, threadIdx.x, P.flag_local[par * W + threadIdx.x]);
+#endif
+  if (s_timeout && threadIdx.x == 0) {
+    P.g->error = 7;  // PGM_ESTATE: a peer never arrived
+    P.g->active = 0;
+    P.g->done = 1;
+  }
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < W; ++q) s += __ldcv(P.win_local + ((size_t)par * W + q) * PEER_NV + v);
+    red[v] = s;
+  }
+  __syncthreads();
+}
+
+// The reduction tail shared by every reduction kernel: local grid reduction,
+// then either the finisher (one GPU, or peer mode after the fused allreduce)
+// or red_out for the host-side collective (NCCL / loopback) + k_finish.
+// Returns true in the block that must run the finisher on red.
+__device__ __forceinline__ bool reduce_tail(const double* bvals, int nv, const Params& P,
+                                            double* red, int G, int bid) {
+  if (!grid_reduce_ex(bvals, nv, P, red, G, bid)) return false;
+  if (P.world > 1 && !P.peer) {
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) P.red_out[v] = red[v];
+    return false;
+  }
+  if (P.peer) peer_allreduce(red, nv, P);
+  return true;
 }
 
 // Block-wide sum (fixed order), result broadcast to every thread.

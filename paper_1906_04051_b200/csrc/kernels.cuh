@@ -469,12 +469,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
     pdl_trigger();
     __syncthreads();
     const int G = SEG ? A.ntiles : (int)gridDim.x;
-    if (P.world > 1) {
-      if (grid_reduce_ex(bvals, nv, P, red, G, tile))
-        for (int v = threadIdx.x; v < nv; v += blockDim.x) P.red_out[v] = red[v];
-      return;
-    }
-    if (grid_reduce_ex(bvals, nv, P, red, G, tile)) E.finish(P, red);
+    if (reduce_tail(bvals, nv, P, red, G, tile)) E.finish(P, red);
     return;
   }
   if constexpr (std::is_same<Epi, PushEpi>::value) {
@@ -526,12 +521,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
     pdl_trigger();
     __syncthreads();
     const int G = SEG ? A.ntiles : (int)gridDim.x;
-    if (P.world > 1) {
-      if (grid_reduce_ex(bvals, nv, P, red, G, tile))
-        for (int v = threadIdx.x; v < nv; v += blockDim.x) P.red_out[v] = red[v];
-      return;
-    }
-    if (grid_reduce_ex(bvals, nv, P, red, G, tile)) E.finish(P, red);
+    if (reduce_tail(bvals, nv, P, red, G, tile)) E.finish(P, red);
     return;
   }
   double acc[NVL];
@@ -550,12 +540,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
   if (nv == 0) return;
   warps_to_block(acc, nv, wacc, bvals);
   const int G = SEG ? A.ntiles : (int)gridDim.x;
-  if (P.world > 1) {
-    if (grid_reduce_ex(bvals, nv, P, red, G, tile))
-      for (int v = threadIdx.x; v < nv; v += blockDim.x) P.red_out[v] = red[v];
-    return;
-  }
-  if (grid_reduce_ex(bvals, nv, P, red, G, tile)) E.finish(P, red);
+  if (reduce_tail(bvals, nv, P, red, G, tile)) E.finish(P, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -806,12 +791,7 @@ __global__ void __launch_bounds__(SW_BLOCK) k_sweep(Params P, int k) {
   }
   if (nv == 0) return;
   warps_to_block(acc, nv, wacc, bvals);
-  if (P.world > 1) {
-    if (grid_reduce(bvals, nv, P, red))
-      for (int vv = threadIdx.x; vv < nv; vv += blockDim.x) P.red_out[vv] = red[vv];
-    return;
-  }
-  if (grid_reduce(bvals, nv, P, red)) sweep_finish<MODE>(P, k, red);
+  if (reduce_tail(bvals, nv, P, red, (int)gridDim.x, (int)blockIdx.x)) sweep_finish<MODE>(P, k, red);
 }
 
 // RPL consecutive rows of one vector (16-byte aligned for RPL >= 2), or zeros.
@@ -989,12 +969,7 @@ __global__ void __launch_bounds__(NW * 32) k_cgs2(Params P, int k, int rev) {
     }
   }
   __syncthreads();
-  if (P.world > 1) {
-    if (grid_reduce(bv, nv, P, redv))
-      for (int vv = threadIdx.x; vv < nv; vv += blockDim.x) P.red_out[vv] = redv[vv];
-    return;
-  }
-  if (grid_reduce(bv, nv, P, redv)) sweep_finish<MODE>(P, k, redv);
+  if (reduce_tail(bv, nv, P, redv, (int)gridDim.x, (int)blockIdx.x)) sweep_finish<MODE>(P, k, redv);
 }
 
 // CGS2 pass C: W_{k+1} = w1 + sum_l b_l W_l (b_l = -h2_l s_l).  No reduction:

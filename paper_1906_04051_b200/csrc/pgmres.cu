@@ -167,6 +167,13 @@ struct pgm_context {
   pgm_deflator* cur_defl = nullptr;  // deflator of the running solve (halo of u)
   double* halo_ptr = nullptr;        // HV_PTR: ctx-layout view of a caller vector (Newton u)
   std::vector<pgm_matrix*> mats;     // live matrices (detached when the context dies first)
+  // fused peer-memory allreduce (common.cuh peer_allreduce): one allocation
+  // holding the window [2][world][PEER_NV] doubles + flags [2][world] + epoch
+  bool peer = false;
+  char* pbuf = nullptr;
+  double** d_peer_win = nullptr;
+  unsigned long long** d_peer_flag = nullptr;
+  std::vector<void*> peer_opened;  // IPC mappings to close
   // optional per-launch profiling (CUDA events around every hot-path kernel)
   bool prof_on = false;
   bool pdl = true;  // programmatic dependent launch of the hot-path kernels (PGMRES_PDL=0 disables)
@@ -608,6 +615,31 @@ Status defl_ensure_hist(pgm_deflator* d, int need) {
   return {};
 }
 
+size_t peer_win_bytes(const pgm_context* ctx) {
+  return sizeof(double) * 2 * (size_t)ctx->world * PEER_NV;
+}
+size_t peer_buf_bytes(const pgm_context* ctx) {
+  return peer_win_bytes(ctx) + sizeof(unsigned long long) * (2 * (size_t)ctx->world + 2);
+}
+
+// Peer-pointer tables: wins[q] / flags[q] = rank q's window and flags as
+// addressable from this rank.
+Status peer_set_tables(pgm_context* ctx, const std::vector<char*>& bufs) {
+  const int W = ctx->world;
+  std::vector<double*> w(W);
+  std::vector<unsigned long long*> f(W);
+  for (int q = 0; q < W; ++q) {
+    w[q] = reinterpret_cast<double*>(bufs[q]);
+    f[q] = reinterpret_cast<unsigned long long*>(bufs[q] + peer_win_bytes(ctx));
+  }
+  if (!ctx->d_peer_win) TRY(dalloc(&ctx->d_peer_win, W));
+  if (!ctx->d_peer_flag) TRY(dalloc(&ctx->d_peer_flag, W));
+  CU(cudaMemcpy(ctx->d_peer_win, w.data(), sizeof(double*) * W, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->d_peer_flag, f.data(), sizeof(void*) * W, cudaMemcpyHostToDevice));
+  ctx->peer = true;
+  return {};
+}
+
 Params make_params(pgm_context* ctx, pgm_deflator* d) {
   Params P{};
   P.g = ctx->g;
@@ -656,6 +688,16 @@ Params make_params(pgm_context* ctx, pgm_deflator* d) {
   P.cnt = ctx->cnt;
   P.red_out = ctx->red_out;
   P.world = ctx->coll ? std::max(ctx->world, 2) : 1;
+  P.peer = ctx->peer ? 1 : 0;
+  P.rank = ctx->rank;
+  P.peer_win = ctx->d_peer_win;
+  P.peer_flag = ctx->d_peer_flag;
+  if (ctx->pbuf) {
+    P.win_local = reinterpret_cast<const double*>(ctx->pbuf);
+    P.flag_local = reinterpret_cast<const unsigned long long*>(ctx->pbuf + peer_win_bytes(ctx));
+    P.epoch = reinterpret_cast<unsigned long long*>(ctx->pbuf + peer_win_bytes(ctx)) +
+              2 * ctx->world;
+  }
   return P;
 }
 
@@ -682,7 +724,7 @@ Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot = 0, cudaStream_t
 
 template <int KIND>
 Status finish_global(pgm_context* ctx, const Params& P, int k, int nv) {
-  if (!ctx->coll) return {};
+  if (!ctx->coll || ctx->peer) return {};  // peer mode: all-reduced inside the kernel
   if (nv <= 0 || nv > ctx->nvmax) return Status{PGM_ESTATE, "finish_global: bad reduction size"};
   TRY(allreduce_red(ctx, nv));
   k_finish<KIND><<<1, 32, 0, ctx->stream>>>(P, k);
@@ -847,6 +889,14 @@ Status solve_impl(pgm_context* ctx, pgm_matrix* A, pgm_deflator* dflt, const dou
   gs.breakdown_scale = cfg->breakdown_scale;
   CU(cudaMemcpyAsync(ctx->g, &gs, sizeof(GState), cudaMemcpyHostToDevice, ctx->stream));
   const Params P = make_params(ctx, d);
+  // In-process peer ranks share one GPU: a device-synchronising call on one
+  // rank (cudaFree, ...) would wait for another rank's kernel spinning on the
+  // first rank's reductions.  Every rank finishes its set-up before any
+  // launches a reduction kernel.
+  if (ctx->loop && ctx->peer) {
+    CU(cudaStreamSynchronize(ctx->stream));
+    ctx->loop->barrier();
+  }
   ctx->cur_defl = d;
   ctx->launches = 0;
   ctx->prof.clear();
@@ -1226,12 +1276,37 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) 
   cudaMemset(ctx->tmp, 0, 8 * ctx->ld);
   if ((s = ensure_reduction(ctx, 2 * MAX_R1 + MAX_M + 8)).code) return bail(s);
   if ((s = set_gstate_idle(ctx)).code) return bail(s);
+  if (cfg->world > 1) {
+    if ((s = dalloc(&ctx->pbuf, peer_buf_bytes(ctx))).code) return bail(s);
+    if (cudaMemset(ctx->pbuf, 0, peer_buf_bytes(ctx)) != cudaSuccess)
+      return bail(Status{PGM_ECUDA, "cudaMemset(peer window)"});
+  }
   if (cfg->world > 1 && cfg->loopback) {
     pgm_loopback* L = static_cast<pgm_loopback*>(cfg->loopback);
     if (L->world != cfg->world) return bail(Status{PGM_EINVAL, "loopback group size != world"});
     ctx->loop = L;
-    std::lock_guard<std::mutex> lk(L->mu);
-    L->ctx[cfg->rank] = ctx;
+    {
+      std::lock_guard<std::mutex> lk(L->mu);
+      L->ctx[cfg->rank] = ctx;
+    }
+    // in-process ranks: the fused peer-memory allreduce with plain pointers
+    // (PGMRES_PEER=0 keeps the host-staged loopback collective instead).  PDL
+    // off: an early-launched next kernel could hold the SMs a spinning peer
+    // rank on the same GPU needs.
+    ctx->pdl = false;
+    // Spinning peers need every kernel resident without a context-wide module
+    // load in between: peer mode only with CUDA_MODULE_LOADING=EAGER (lazy
+    // loading of a kernel's module waits for the other ranks' spinning kernels).
+    const char* pe = std::getenv("PGMRES_PEER");
+    const char* ml = std::getenv("CUDA_MODULE_LOADING");
+    const bool want_peer = !(pe && pe[0] == '0') && ml && std::string(ml) == "EAGER";
+    L->barrier();  // every rank registered and has its window
+    if (want_peer) {
+      std::vector<char*> bufs(cfg->world);
+      for (int q = 0; q < cfg->world; ++q) bufs[q] = L->ctx[q]->pbuf;
+      if ((s = peer_set_tables(ctx, bufs)).code) return bail(s);
+    }
+    L->barrier();
   } else if (cfg->world > 1 || cfg->nccl_id) {
     if (!nccl_lite::available()) return bail(Status{PGM_ENCCL, "libnccl.so.2 not loadable"});
     if (!cfg->nccl_id) return bail(Status{PGM_EINVAL, "world > 1 needs an ncclUniqueId"});
@@ -1260,6 +1335,11 @@ void pgm_context_destroy(pgm_context* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (pgm_matrix* m : ctx->mats) m->ctx = nullptr;  // destroyed later with plain frees
   ctx->mats.clear();
+  for (void* p : ctx->peer_opened) cudaIpcCloseMemHandle(p);
+  ctx->peer_opened.clear();
+  dfree(ctx->d_peer_win);
+  dfree(ctx->d_peer_flag);
+  dfree(ctx->pbuf);
   if (ctx->dummy) pgm_deflator_destroy(ctx->dummy);
   free_workspace(ctx);
   dfree(ctx->x);
@@ -1775,6 +1855,49 @@ Status bratu_assemble(pgm_context* ctx, uint32_t n_e, double lambda, const doubl
 }  // namespace
 
 extern "C" {
+
+pgm_status pgm_peer_export(pgm_context* ctx, void* out128) {
+  if (!ctx || !out128) return PGM_EINVAL;
+  if (ctx->world < 2 || !ctx->pbuf)
+    return fail(ctx, einval("pgm_peer_export: needs a world > 1 context"));
+  cudaSetDevice(ctx->device);
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ctx->pbuf);
+  if (e != cudaSuccess) return fail(ctx, Status{PGM_ECUDA, std::string("cudaIpcGetMemHandle: ") +
+                                                             cudaGetErrorString(e)});
+  std::memset(out128, 0, 128);
+  std::memcpy(out128, &h, sizeof(h));
+  return PGM_OK;
+}
+
+pgm_status pgm_peer_import(pgm_context* ctx, const void* all) {
+  if (!ctx || !all) return PGM_EINVAL;
+  if (ctx->world < 2 || !ctx->pbuf || ctx->loop)
+    return fail(ctx, einval("pgm_peer_import: needs a world > 1 NCCL context"));
+  const char* ml = std::getenv("CUDA_MODULE_LOADING");
+  if (!ml || std::string(ml) != "EAGER")
+    return fail(ctx, einval("pgm_peer_import: set CUDA_MODULE_LOADING=EAGER before CUDA starts "
+                            "(lazy module loading can stall spinning peer kernels)"));
+  cudaSetDevice(ctx->device);
+  std::vector<char*> bufs(ctx->world);
+  for (int q = 0; q < ctx->world; ++q) {
+    if (q == ctx->rank) {
+      bufs[q] = ctx->pbuf;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(all) + 128 * (size_t)q, sizeof(h));
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return fail(ctx, Status{PGM_ECUDA, std::string("cudaIpcOpenMemHandle: ") +
+                                             cudaGetErrorString(e)});
+    ctx->peer_opened.push_back(p);
+    bufs[q] = static_cast<char*>(p);
+  }
+  Status s = peer_set_tables(ctx, bufs);
+  return s.code ? fail(ctx, s) : PGM_OK;
+}
 
 pgm_status pgm_nccl_unique_id(void* out128) {
   if (!out128) return PGM_EINVAL;

@@ -207,6 +207,21 @@ class DeviceExecutor:
         self._ctx = h
         self.n_global = int(n_global)
 
+    # ---- peer-memory transport (pgm_peer_export / pgm_peer_import) ----
+    def peer_export(self) -> bytes:
+        """This rank's 128-byte window handle (gather all ranks', then peer_import)."""
+        buf = C.create_string_buffer(128)
+        _check(capi.lib().pgm_peer_export(self.handle, buf), self.handle)
+        return buf.raw
+
+    def peer_import(self, handles) -> None:
+        """handles: the world ranks' peer_export() blobs in rank order."""
+        blob = b"".join(bytes(h) for h in handles)
+        if len(blob) != 128 * self.world:
+            raise ValueError("peer_import needs world x 128 bytes")
+        buf = C.create_string_buffer(blob, len(blob))
+        _check(capi.lib().pgm_peer_import(self.handle, buf), self.handle)
+
     def _ensure(self, n_global: int):
         if self._ctx is None:
             self._create(n_global)

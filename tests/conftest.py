@@ -1,7 +1,13 @@
 import os
 import sys
 
-import pytest
+# Before CUDA starts: eager module loading (the in-kernel peer-memory allreduce
+# of the multi-rank tests needs every kernel loaded up front) and enough
+# hardware queues that in-process ranks' streams do not serialise.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+import pytest  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:

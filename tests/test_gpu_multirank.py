@@ -1,8 +1,10 @@
 """GPU: the multi-rank path (z-slab rows, halo planes, per-reduction allreduce
 + replicated finisher) run as W ranks on ONE GPU through the in-process
-loopback communicator (one host thread per rank).  Only the NCCL transport is
-replaced; kernels, partition (partition_rows, parallel.cpp:50-71) and
-collective placement are the production world > 1 code."""
+loopback communicator (one host thread per rank).  Kernels, partition
+(partition_rows, parallel.cpp:50-71) and collective placement are the
+production world > 1 code; the allreduce runs either fused inside the
+reduction kernels over peer memory (the in-kernel protocol used with CUDA IPC
+windows across GPUs) or host-staged in place of NCCL."""
 import threading
 
 import numpy as np
@@ -19,6 +21,15 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch
+
+
+@pytest.fixture(params=["peer", "host"])
+def transport(request, monkeypatch):
+    """peer: the fused in-kernel allreduce over peer memory (default for
+    in-process ranks); host: the host-staged loopback collective (the NCCL
+    code path's allreduce_red + k_finish placement)."""
+    monkeypatch.setenv("PGMRES_PEER", "1" if request.param == "peer" else "0")
+    return request.param
 
 
 def run_ranks(world, fn):
@@ -62,7 +73,7 @@ def test_multirank_spmv_bitexact(cuda, ref, world):
 
 
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_multirank_deflated_cfg1(cuda, golden, world):
+def test_multirank_deflated_cfg1(cuda, golden, world, transport):
     ne = 10
     na = 2 * ne + 1
     g = golden("cfg1_defl")
@@ -90,7 +101,7 @@ def test_multirank_deflated_cfg1(cuda, golden, world):
     assert res[0][2] == int(g["rank"])
 
 
-def test_multirank_truncation_run(cuda, golden):
+def test_multirank_truncation_run(cuda, golden, transport):
     ne, world = 10, 2
     na = 2 * ne + 1
     g = golden("ne10_m4_trunc")
