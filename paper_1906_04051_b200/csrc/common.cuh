@@ -253,12 +253,21 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __noinline__ void peer_allreduce(double* red, int nv, const Params& P) {
+#ifndef PGM_PEER_INLINE
+#define PGM_PEER_INLINE __noinline__
+#endif
+// (noinline, arguments by value: the hot kernels keep their register
+// allocation and do not spill Params to the stack for the call)
+__device__ PGM_PEER_INLINE void peer_allreduce_impl(double* red, int nv, int W, int me,
+                                                 double* const* peer_win,
+                                                 unsigned long long* const* peer_flag,
+                                                 const double* win_local,
+                                                 const unsigned long long* flag_local,
+                                                 unsigned long long* epoch, GState* g) {
   __shared__ unsigned long long s_e;
   __shared__ int s_timeout;
-  const int W = P.world, me = P.rank;
   if (threadIdx.x == 0) {
-    s_e = ++(*P.epoch);
+    s_e = ++(*epoch);
     s_timeout = 0;
   }
   __syncthreads();
@@ -268,14 +277,14 @@ __device__ __noinline__ void peer_allreduce(double* red, int nv, const Params& P
   if (threadIdx.x == 0 && e < 12) printf("peer rank %d e %llu nv %d grid %d\n", me, e, nv, (int)gridDim.x);
 #endif
   for (int q = 0; q < W; ++q) {
-    double* dst = P.peer_win[q] + ((size_t)par * W + me) * PEER_NV;
+    double* dst = peer_win[q] + ((size_t)par * W + me) * PEER_NV;
     for (int v = threadIdx.x; v < nv; v += blockDim.x) dst[v] = red[v];
   }
   __threadfence_system();
   __syncthreads();
-  if (threadIdx.x < W) st_release_sys(P.peer_flag[threadIdx.x] + par * W + me, e);
+  if (threadIdx.x < W) st_release_sys(peer_flag[threadIdx.x] + par * W + me, e);
   if (threadIdx.x < W) {
-    const unsigned long long* f = P.flag_local + par * W + threadIdx.x;
+    const unsigned long long* f = flag_local + par * W + threadIdx.x;
     long long spins = 0;
     while (ld_acquire_sys(f) < e) {
       if (++spins > (1ll << 24)) {  // ~10 s
@@ -287,19 +296,24 @@ __device__ __noinline__ void peer_allreduce(double* red, int nv, const Params& P
   __syncthreads();
 #ifdef PGM_PEER_DEBUG
   if (s_timeout && threadIdx.x == 0) printf("peer TIMEOUT rank %d e %llu\n", me, e);
-  if (threadIdx.x < W && e < 12) printf("peer rank %d sees flag[%d] = %llu\n", me, threadIdx.x, P.flag_local[par * W + threadIdx.x]);
+  if (threadIdx.x < W && e < 12) printf("peer rank %d sees flag[%d] = %llu\n", me, threadIdx.x, flag_local[par * W + threadIdx.x]);
 #endif
   if (s_timeout && threadIdx.x == 0) {
-    P.g->error = 7;  // PGM_ESTATE: a peer never arrived
-    P.g->active = 0;
-    P.g->done = 1;
+    g->error = 7;  // PGM_ESTATE: a peer never arrived
+    g->active = 0;
+    g->done = 1;
   }
   for (int v = threadIdx.x; v < nv; v += blockDim.x) {
     double s = 0.0;
-    for (int q = 0; q < W; ++q) s += __ldcv(P.win_local + ((size_t)par * W + q) * PEER_NV + v);
+    for (int q = 0; q < W; ++q) s += __ldcv(win_local + ((size_t)par * W + q) * PEER_NV + v);
     red[v] = s;
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ void peer_allreduce(double* red, int nv, const Params& P) {
+  peer_allreduce_impl(red, nv, P.world, P.rank, P.peer_win, P.peer_flag, P.win_local,
+                      P.flag_local, P.epoch, P.g);
 }
 
 // The reduction tail shared by every reduction kernel: local grid reduction,
