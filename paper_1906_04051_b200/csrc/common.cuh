@@ -118,9 +118,6 @@ constexpr int PEER_NV = 2 * MAX_R1 + MAX_M + 8;  // values per reduction slot
 #ifndef PGM_PDL_ASM
 #define PGM_PDL_ASM 1
 #endif
-#ifndef PGM_SPMV_REV
-#define PGM_SPMV_REV 0
-#endif
 #ifndef PGM_SPMV_EARLY_PF
 #define PGM_SPMV_EARLY_PF 1
 #endif

@@ -38,7 +38,6 @@ struct Sell {
   const unsigned* lane_base;       // compressed: first column of the lane's row
   int ntiles;
   int n;
-  int rev;  // walk the tiles from the last one (L2 reuse of the previous kernel's tail)
 };
 
 // Slice layout: entry (lane, t) of a slice lives at base + (t/4)*128 + lane*4 + t%4,
@@ -547,7 +546,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
 // Streaming sweeps over basis blocks.
 enum SweepMode {
   SW_CGS2_B = 0,   // w1 = w - V h1 ; dots V^T w1 (staged)
-  SW_CGS2_C = 1,   // w2 = w1 - V h2 ; ||w2||^2, U^T w2
+  SW_CGS2_C = 1,   // w2 = w1 - V h2 (k_cgs2_update; class id for the profile only)
   SW_XUPDATE = 2,  // x += V xc + U cx
   SW_PUSH1 = 3,    // u = V zl (or u given) ; ||u||^2, U^T u
   SW_PUSH2 = 4,    // u -= U proj ; U^T u (staged)
@@ -591,15 +590,6 @@ __device__ __forceinline__ SweepSpec sweep_spec(const Params& P, int k) {
     S.qstaged = 1;
     S.selfnorm = 1;
     S.normlast = 1;
-  } else if (MODE == SW_CGS2_C) {
-    S.skip = !g->active;
-    S.in = S.out = P.V + (size_t)(k + 1) * P.ld + lo;
-    S.Pv = P.V + lo;
-    S.np = k + 1;
-    S.a = P.coefB;
-    S.Q = P.U + lo;
-    S.nq = d->r;
-    S.selfnorm = 1;
   } else if (MODE == SW_XUPDATE) {
     S.skip = g->error != 0;
     S.in = S.out = P.x + lo;
@@ -832,13 +822,10 @@ __device__ __forceinline__ void store_rows(double* p, const double (&o)[RPL]) {
 // depends only on the grid size: bitwise reproducible run to run.
 // Rows past the owned range (padding / halo memory, always allocated) are read
 // and masked before any store or product.
-// rev: walk the chunks from the end of the vectors.  Consecutive hot-path
-// kernels alternate direction, so each one starts on the rows whose basis
-// entries the previous kernel left in the 126 MB L2.
 // NUW: deflation vectors per warp (covers the rank r of this cycle; the host
 // picks the instantiation), NPW: basis vectors per warp.
 template <int MODE, int NW, int RPL, int NUW, int NPW>
-__global__ void __launch_bounds__(NW * 32) k_cgs2(Params P, int k, int rev) {
+__global__ void __launch_bounds__(NW * 32) k_cgs2(Params P, int k) {
   static_assert(MODE == SW_CGS2_B, "pass C is k_cgs2_update");
   constexpr int NA = NPW + NUW + 1;
   constexpr int CR = 32 * RPL;  // rows per chunk
@@ -854,7 +841,7 @@ __global__ void __launch_bounds__(NW * 32) k_cgs2(Params P, int k, int rev) {
   // Ahead of the PDL wait: L2 prefetch of this warp's W_0..W_k segments of its
   // first two chunks (W_l, l <= k, were written >= 2 kernels back).
   for (int c = blockIdx.x; c < nch && c < (int)(blockIdx.x + 2 * gridDim.x); c += gridDim.x) {
-    const size_t off = (size_t)(rev ? nch - 1 - c : c) * CR;
+    const size_t off = (size_t)c * CR;
     for (int q = lane; q < NPW; q += 32) {
       const int l = warp + NW * q;
       if (l < np) tma_prefetch_l2(V0 + (size_t)l * ld + off, CR * 8);
@@ -878,7 +865,7 @@ __global__ void __launch_bounds__(NW * 32) k_cgs2(Params P, int k, int rev) {
   // L2 prefetch (TMA engine) of this warp's segments of chunk c
   auto prefetch = [&](int c) {
     if (c >= nch) return;
-    const size_t off = (size_t)(rev ? nch - 1 - c : c) * CR;
+    const size_t off = (size_t)c * CR;
     for (int q = lane; q < NPW + NUW + 1; q += 32) {
       const double* src = nullptr;
       if (q < NPW) {
@@ -896,7 +883,7 @@ __global__ void __launch_bounds__(NW * 32) k_cgs2(Params P, int k, int rev) {
   int buf = 0;
   for (int c = blockIdx.x; c < nch; c += gridDim.x) {
     prefetch(c + 2 * gridDim.x);
-    const int row0 = (rev ? nch - 1 - c : c) * CR + lane * RPL;
+    const int row0 = c * CR + lane * RPL;
     double v[NPW][RPL];
     double u[NUW > 0 ? NUW : 1][RPL];
     double win[RPL];

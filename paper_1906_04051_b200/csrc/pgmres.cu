@@ -216,7 +216,6 @@ struct pgm_matrix {
     S.lane_base = lane_base;
     S.ntiles = ntiles;
     S.n = (int)n;
-    S.rev = 0;
     return S;
   }
 };
@@ -401,25 +400,25 @@ Status launch_sweep_np(pgm_context* ctx, const Params& P, int k, int nv, int np)
 // CGS2 sweeps (np = k + 1): warp-split kernels; 4 warps per block (8 above
 // 64 vectors), 2 rows per lane (tools/sweepbench.cu, tools/run_variants.sh).
 template <int MODE, int NW, int RPL, int NUW, int NPW>
-Status launch_cgs2_cfg(pgm_context* ctx, const Params& P, int k, int rev) {
+Status launch_cgs2_cfg(pgm_context* ctx, const Params& P, int k) {
   static int occ = 0;  // per instantiation; same device geometry for every context
   if (occ == 0)
     occ = std::min(MAX_SPLIT_BLOCKS_PER_SM, occupancy(k_cgs2<MODE, NW, RPL, NUW, NPW>, NW * 32, 0));
   const int nchunks = (int)((ctx->n + 32 * RPL - 1) / (32 * RPL));
   const int G = std::max(1, std::min(nchunks, occ * ctx->nsm));
   ProfScope ps(ctx, prof_class_sweep<MODE>(), (uint32_t)k);
-  CU(launch_pdl(ctx, k_cgs2<MODE, NW, RPL, NUW, NPW>, G, NW * 32, 0, P, k, rev));
+  CU(launch_pdl(ctx, k_cgs2<MODE, NW, RPL, NUW, NPW>, G, NW * 32, 0, P, k));
   ctx->launches++;
   CU(cudaGetLastError());
   return {};
 }
 
 template <int MODE, int NW, int RPL, int NUW, int... Is>
-Status launch_cgs2_table(pgm_context* ctx, const Params& P, int k, int rev, int npw,
+Status launch_cgs2_table(pgm_context* ctx, const Params& P, int k, int npw,
                          std::integer_sequence<int, Is...>) {
-  using Fn = Status (*)(pgm_context*, const Params&, int, int);
+  using Fn = Status (*)(pgm_context*, const Params&, int);
   static constexpr Fn table[] = {&launch_cgs2_cfg<MODE, NW, RPL, NUW, Is + 1>...};
-  return table[npw - 1](ctx, P, k, rev);
+  return table[npw - 1](ctx, P, k);
 }
 
 constexpr int CGS2_SPLIT_MAX = 112;  // = MAX_M: 8 warps x 14 vectors
@@ -444,33 +443,33 @@ Status launch_cgs2_update(pgm_context* ctx, const Params& P, int k) {
 // r (constant within a cycle; read with the restart status word), so early
 // cycles with a small basis do not pay registers for U.
 template <int NW, int R, int NUW, int NPWMAX>
-Status launch_cgs2_nuw(pgm_context* ctx, const Params& P, int k, int rev, int npw) {
-  return launch_cgs2_table<SW_CGS2_B, NW, R, NUW>(ctx, P, k, rev, npw,
+Status launch_cgs2_nuw(pgm_context* ctx, const Params& P, int k, int npw) {
+  return launch_cgs2_table<SW_CGS2_B, NW, R, NUW>(ctx, P, k, npw,
                                                   std::make_integer_sequence<int, NPWMAX>{});
 }
 
 template <int NW, int R, int NPWMAX>
-Status launch_cgs2_r(pgm_context* ctx, const Params& P, int k, int rev, int npw, int r) {
+Status launch_cgs2_r(pgm_context* ctx, const Params& P, int k, int npw, int r) {
   const int nuw = (r + NW - 1) / NW;
-  if (nuw == 0) return launch_cgs2_nuw<NW, R, 0, NPWMAX>(ctx, P, k, rev, npw);
-  if (nuw <= 1) return launch_cgs2_nuw<NW, R, 1, NPWMAX>(ctx, P, k, rev, npw);
-  if (nuw <= 2) return launch_cgs2_nuw<NW, R, 2, NPWMAX>(ctx, P, k, rev, npw);
-  if (nuw <= 4) return launch_cgs2_nuw<NW, R, 4, NPWMAX>(ctx, P, k, rev, npw);
+  if (nuw == 0) return launch_cgs2_nuw<NW, R, 0, NPWMAX>(ctx, P, k, npw);
+  if (nuw <= 1) return launch_cgs2_nuw<NW, R, 1, NPWMAX>(ctx, P, k, npw);
+  if (nuw <= 2) return launch_cgs2_nuw<NW, R, 2, NPWMAX>(ctx, P, k, npw);
+  if (nuw <= 4) return launch_cgs2_nuw<NW, R, 4, NPWMAX>(ctx, P, k, npw);
   if constexpr (NW == 4) {
-    if (nuw <= 6) return launch_cgs2_nuw<NW, R, 6, NPWMAX>(ctx, P, k, rev, npw);
+    if (nuw <= 6) return launch_cgs2_nuw<NW, R, 6, NPWMAX>(ctx, P, k, npw);
   }
-  return launch_cgs2_nuw<NW, R, (MAX_R1 + NW - 1) / NW, NPWMAX>(ctx, P, k, rev, npw);
+  return launch_cgs2_nuw<NW, R, (MAX_R1 + NW - 1) / NW, NPWMAX>(ctx, P, k, npw);
 }
 
-Status launch_cgs2_b(pgm_context* ctx, const Params& P, int k, int nv, int rev, int r) {
+Status launch_cgs2_b(pgm_context* ctx, const Params& P, int k, int nv, int r) {
   constexpr int R = PGM_CGS2_RPL;
   const int np = k + 1;
 #ifndef PGM_B_NW
 #define PGM_B_NW 4
 #endif
   constexpr int BNW = PGM_B_NW;
-  if (np <= 64) return launch_cgs2_r<BNW, R, (64 + BNW - 1) / BNW>(ctx, P, k, rev, (np + BNW - 1) / BNW, r);
-  if (np <= CGS2_SPLIT_MAX) return launch_cgs2_r<8, R, 14>(ctx, P, k, rev, (np + 7) / 8, r);
+  if (np <= 64) return launch_cgs2_r<BNW, R, (64 + BNW - 1) / BNW>(ctx, P, k, (np + BNW - 1) / BNW, r);
+  if (np <= CGS2_SPLIT_MAX) return launch_cgs2_r<8, R, 14>(ctx, P, k, (np + 7) / 8, r);
   return launch_sweep_np<SW_CGS2_B, 0>(ctx, P, k, nv, np);
 }
 
@@ -755,18 +754,18 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
       CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo_done, 0));
       TRY(launch_spmv(ctx, A, P, se, m + 1, (uint32_t)k, 2));
       TRY(finish_global<100>(ctx, P, k, k + 1));
-      TRY(launch_cgs2_b(ctx, P, k, k + 2 + R1, 0, ctx->cur_defl ? ctx->h_dstate->r : R1));
+      TRY(launch_cgs2_b(ctx, P, k, k + 2 + R1, ctx->cur_defl ? ctx->h_dstate->r : R1));
       TRY(finish_global<SW_CGS2_B>(ctx, P, k, k + 2 + R1));
       TRY(launch_cgs2_update(ctx, P, k));
       continue;
     }
     if (ctx->world > 1) TRY(halo_exchange(ctx, HV_V, k));
-    // rev = 0: alternating the walk direction per kernel (to reuse the
-    // previous kernel's L2 tail) measured slower on B200 (tools/prof_by_k.py)
+    // (alternating the walk direction kernel to kernel, to reuse the previous
+    // kernel's L2 tail, measured slower on B200: all kernels walk forward)
     StepEpi se{k};
     TRY(launch_spmv(ctx, A, P, se, m + 1, (uint32_t)k));
     TRY(finish_global<100>(ctx, P, k, k + 1));
-    TRY(launch_cgs2_b(ctx, P, k, k + 2 + R1, 0, ctx->cur_defl ? ctx->h_dstate->r : R1));
+    TRY(launch_cgs2_b(ctx, P, k, k + 2 + R1, ctx->cur_defl ? ctx->h_dstate->r : R1));
     TRY(finish_global<SW_CGS2_B>(ctx, P, k, k + 2 + R1));
     TRY(launch_cgs2_update(ctx, P, k));
   }
