@@ -1136,10 +1136,9 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
     return;
   }
   const double tol = d->inv_tol;
-  // ---- largest_ritz_value: power iteration (deflation.cpp:57-82).  Block
-  // sums with one barrier each (rotating slot arrays), the H z buffer swaps
-  // roles with the iterate instead of being copied: 5 barriers per iteration.
-  __shared__ double sA[RITZ_THREADS / 32], sB[RITZ_THREADS / 32], sC[RITZ_THREADS / 32];
+  // ---- largest_ritz_value: power iteration (deflation.cpp:57-82); block
+  // sums with one barrier each (separate slot arrays per sum).
+  __shared__ double sA[RITZ_THREADS / 32], sB[RITZ_THREADS / 32];
   auto bsum1 = [&](double v, double* slots) {
     v = warp_sum(v);
     if ((tid & 31) == 0) slots[tid >> 5] = v;
@@ -1149,44 +1148,58 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
     return t;
   };
   {
-    double* it_x = nx;  // H z of the current iterate
-    double* it_h = hz;
+    // y = H z_{i-1} (unnormalised iterate), hy = H y.  One fused sum gives
+    // y.y and y.hy (nz = |y|, theta = y.hy / y.y = z.Hz), the second
+    // |hy - theta y|^2 / y.y (= |Hz - theta z|^2) while y <- hy / nz is
+    // written for the next iteration: 3 barriers and 2 reductions per step.
+    __shared__ double sA2[RITZ_THREADS / 32];
+    double* y = nx;
+    double* hy = hz;
     for (int i = tid; i < k; i += blockDim.x) z[i] = 1.0 / sqrt((double)k);
     __syncthreads();
-    hmatvec(H, k, z, it_x);
+    hmatvec(H, k, z, y);
     __syncthreads();
     bool have = false, conv = false, broke = false;
     double val = 0.0;
     for (int it = 0; it < d->pow_maxit; ++it) {
-      double p = 0.0;
-      for (int i = tid; i < k; i += blockDim.x) p += it_x[i] * it_x[i];
-      const double nz = sqrt(bsum1(p, sA));
+      hmatvec(H, k, y, hy);
+      __syncthreads();
+      double p = 0.0, q = 0.0;
+      for (int i = tid; i < k; i += blockDim.x) {
+        p += y[i] * y[i];
+        q += y[i] * hy[i];
+      }
+      p = warp_sum(p);
+      q = warp_sum(q);
+      if ((tid & 31) == 0) {
+        sA[tid >> 5] = p;
+        sA2[tid >> 5] = q;
+      }
+      __syncthreads();
+      double yy = 0.0, yhy = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        yy += sA[w];
+        yhy += sA2[w];
+      }
+      const double nz = sqrt(yy);
       if (!isfinite(nz) || nz == 0.0) {
         broke = true;
         break;
       }
-      for (int i = tid; i < k; i += blockDim.x) z[i] = it_x[i] / nz;
-      __syncthreads();
-      hmatvec(H, k, z, it_h);
-      __syncthreads();
-      double q = 0.0;
-      for (int i = tid; i < k; i += blockDim.x) q += z[i] * it_h[i];
-      const double theta = bsum1(q, sB);
+      const double theta = yhy / yy;
       double e = 0.0;
       for (int i = tid; i < k; i += blockDim.x) {
-        const double t = it_h[i] - theta * z[i];
+        const double t = hy[i] - theta * y[i];
         e += t * t;
+        y[i] = hy[i] / nz;  // H z_i for the next iteration
       }
-      const double resid = sqrt(bsum1(e, sC));
+      const double resid = sqrt(bsum1(e, sB) / yy);
       val = theta;
       have = true;
       if (resid <= tol * scale) {
         conv = true;
         break;
       }
-      double* t = it_x;  // H z of the new z
-      it_x = it_h;
-      it_h = t;
     }
     const bool ok = conv || (!broke && have);
     if (tid == 0 && ok && isfinite(val) && fabs(val) > fabs(d->mu)) d->mu = val;  // observe_ritz
@@ -1248,35 +1261,52 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
   }
   load_h();  // H again for theta / residuals
   __syncthreads();
-  // ---- smallest_ritz_pair: inverse power iteration (deflation.cpp:31-54), 6 barriers / it
+  // ---- smallest_ritz_pair: inverse power iteration (deflation.cpp:31-54):
+  // y = H^-1 z, hy = H y; y.y and y.hy in one sum, then the residual while
+  // z <- y / |y| is written: 4 barriers per iteration.
   for (int i = tid; i < k; i += blockDim.x) z[i] = 1.0 / sqrt((double)k);
   __syncthreads();
   bool conv = false;
   double val = 0.0;
-  for (int it = 0; it < d->inv_maxit; ++it) {
-    hmatvec(B, k, z, nx);
-    __syncthreads();
-    double p = 0.0;
-    for (int i = tid; i < k; i += blockDim.x) p += nx[i] * nx[i];
-    const double nz = sqrt(bsum1(p, sA));
-    if (!isfinite(nz) || nz == 0.0) break;
-    for (int i = tid; i < k; i += blockDim.x) z[i] = nx[i] / nz;
-    __syncthreads();
-    hmatvec(H, k, z, hz);
-    __syncthreads();
-    double q = 0.0;
-    for (int i = tid; i < k; i += blockDim.x) q += z[i] * hz[i];
-    const double theta = bsum1(q, sB);
-    double e = 0.0;
-    for (int i = tid; i < k; i += blockDim.x) {
-      const double t = hz[i] - theta * z[i];
-      e += t * t;
-    }
-    const double resid = sqrt(bsum1(e, sC));
-    val = theta;
-    if (resid <= tol * scale) {
-      conv = true;
-      break;
+  {
+    __shared__ double sA3[RITZ_THREADS / 32];
+    for (int it = 0; it < d->inv_maxit; ++it) {
+      hmatvec(B, k, z, nx);
+      __syncthreads();
+      hmatvec(H, k, nx, hz);
+      __syncthreads();
+      double p = 0.0, q = 0.0;
+      for (int i = tid; i < k; i += blockDim.x) {
+        p += nx[i] * nx[i];
+        q += nx[i] * hz[i];
+      }
+      p = warp_sum(p);
+      q = warp_sum(q);
+      if ((tid & 31) == 0) {
+        sA[tid >> 5] = p;
+        sA3[tid >> 5] = q;
+      }
+      __syncthreads();
+      double yy = 0.0, yhy = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        yy += sA[w];
+        yhy += sA3[w];
+      }
+      const double nz = sqrt(yy);
+      if (!isfinite(nz) || nz == 0.0) break;
+      const double theta = yhy / yy;
+      double e = 0.0;
+      for (int i = tid; i < k; i += blockDim.x) {
+        const double t = hz[i] - theta * nx[i];
+        e += t * t;
+        z[i] = nx[i] / nz;
+      }
+      const double resid = sqrt(bsum1(e, sB) / yy);
+      val = theta;
+      if (resid <= tol * scale) {
+        conv = true;
+        break;
+      }
     }
   }
   if (conv) {
