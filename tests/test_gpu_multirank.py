@@ -120,3 +120,27 @@ def test_multirank_truncation_run(cuda, golden, transport):
     assert res[0][2] == list(g["hist_r"])
     assert np.abs(res[0][3] - g["T"]).max() <= 1e-8 * np.abs(g["T"]).max()
     assert np.linalg.norm(x - g["x"]) <= 1e-8 * np.linalg.norm(g["x"])
+
+
+def test_multirank_newton_ne8(cuda, golden, transport):
+    """The device-resident Newton driver on 2 z-slab ranks: every rank
+    assembles its rows from the global iterate, solves its share and keeps
+    its halo planes of u current; result identical to the reference's."""
+    ne, world = 8, 2
+    na = 2 * ne + 1
+    g = golden("newton_ne8")
+
+    def rank(r, grp):
+        ex = pg.DeviceExecutor(0, n_global=na ** 3, n_axis=na, rank=r, world=world, loopback=grp)
+        u = np.zeros(na ** 3)
+        rep = pg.newton_solve(ne, 6.8, u, pg.NewtonConfig(), ex)
+        p = ex.partition()
+        return rep, u[p["row_begin"]:p["row_end"]].copy()
+
+    res = run_ranks(world, rank)
+    u = np.concatenate([rr[1] for rr in res])
+    rep = res[0][0]
+    assert rep.converged and len(rep.iters) == len(g["inner"])
+    assert [it.gmres_inner for it in rep.iters] == [it.gmres_inner for it in res[1][0].iters]
+    assert np.all(np.abs(np.array([it.gmres_inner for it in rep.iters]) - g["inner"]) <= 3)
+    assert np.linalg.norm(u - g["u"]) <= 1e-8 * np.linalg.norm(g["u"])
