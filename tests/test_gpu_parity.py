@@ -470,3 +470,30 @@ def test_cfg3_deflated_full_size(torch_cuda, golden):
     hr = np.array([h.r for h in d.history()])
     k = min(len(hr), len(g["hist_r"]))
     assert np.array_equal(hr[:k], g["hist_r"][:k]), (hr, g["hist_r"])
+
+
+@pytest.mark.parametrize("m,defl", [(20, True), (20, False), (100, True), (100, False)])
+def test_restart_length_sweep_ne25(torch_cuda, golden, m, defl):
+    """BASELINE config 5's restart sweep (m in {20, 50, 100}, deflation on and
+    off; m = 50 is cfg2) on n_e = 25 against the reference
+    (tests/golden/make_golden_sweep.py).  m = 100 runs the 8-warp pass-B
+    kernels (more than 64 basis vectors)."""
+    g = golden("sweep_ne25")
+    key = f"m{m}_{'defl' if defl else 'plain'}"
+    ex = pg.DeviceExecutor()
+    A, b = ex.assemble_bratu(25, 6.8, device=True)
+    x = torch_cuda.zeros(ex.n_own, dtype=torch_cuda.float64, device="cuda")
+    cfg = pg.GmresConfig(m=m, max_restarts=200, rel_tol=1e-10)
+    if defl:
+        rep = pg.deflated_gmres(A, b, x, cfg, pg.Deflator(pg.DeflationConfig(), ex), ex)
+    else:
+        rep = pg.gmres_restarted(A, None, b, x, cfg, ex)
+    b0 = float(g[key + "_beta0"])
+    assert rep.converged
+    assert abs(rep.total_inner - int(g[key + "_total_inner"])) <= 1
+    n = min(len(rep.monitored), len(g[key + "_monitored"]))
+    assert np.max(np.abs(rep.monitored[:n] - g[key + "_monitored"][:n])) <= HIST_TOL * b0
+    xh = x.cpu().numpy()
+    assert abs(np.linalg.norm(xh) - float(g[key + "_x_norm"])) <= X_TOL * float(g[key + "_x_norm"])
+    assert np.linalg.norm(xh[::97] - g[key + "_x_sample"]) <= 10 * X_TOL * np.linalg.norm(
+        g[key + "_x_sample"])
