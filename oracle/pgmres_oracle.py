@@ -21,6 +21,10 @@ Each function restates one reference routine (file:line into
 `orth="cgs2"` switches arnoldi_step to the unconditional two-pass classical
 Gram-Schmidt the device path runs (SURVEY.md §8(c) shows it keeps parity), so
 tests can separate "algorithm variant" from "rounding" differences.
+`orth="dcgs2"` is a numerical prototype of delayed CGS2 (a
+candidate device algorithm): the SpMV runs on the lagged once-orthogonalised
+vector and the reorthogonalisation + Arnoldi correction happen one step
+later; tests/test_oracle.py measures its parity before any device code.
 
 Parity of this restatement is PINNED against the reference itself: the
 golden fixtures in tests/golden/ are produced by oracle/_ref (the reference's
@@ -178,6 +182,64 @@ class Workspace:
         return self.h_orig[i, j]
 
 
+def _dcgs2_cycle(ws, opA, opM, cfg, rep, restart, beta_cycle):
+    """One restart cycle of delayed CGS2 (one global reduction per step).
+
+    Step k runs the operator on the lagged vector u_k (orthogonalised once
+    against q_0..q_{k-1}) and, from ONE batch of dot products
+    [Q^T u_k, u_k.u_k, Q^T w, u_k.w], finishes u_k's second pass (column k-1 of
+    H gets + a, h_{k,k-1} = beta) and forms the first pass of the next vector
+    through the Arnoldi relation A M^-1 Q = Q H.  Column k-1's Givens update and
+    termination tests therefore happen at step k; the cycle end needs one
+    closing reduction (no operator application)."""
+    m = ws.m
+    op = (lambda v: opA(opM(v))) if opM is not None else opA
+    Q = ws.V
+    steps, lucky = 0, False
+    # step 0: q_0 is final
+    w = np.array(op(Q[0]), copy=True)
+    h1 = np.array([float(Q[0] @ w)])
+    u = w - h1[0] * Q[0]
+    ws.h_orig[0, 0] = h1[0]
+    for k in range(1, m + 1):
+        a = Q[:k] @ u
+        alpha = float(u @ u)
+        if k < m:
+            w = np.array(op(u), copy=True)
+            b = Q[:k] @ w
+            gamma = float(u @ w)
+        beta = math.sqrt(max(alpha - float(a @ a), 0.0))
+        if not math.isfinite(beta):
+            raise GmresError(f"gmres: non-finite Arnoldi coefficient at restart {restart}, "
+                             f"step {k - 1}")
+        # column k-1 complete: second-pass coefficients and the subdiagonal
+        ws.h_orig[:k, k - 1] += a
+        ws.h_orig[k, k - 1] = beta
+        ws.h_rot[: k + 1, k - 1] = ws.h_orig[: k + 1, k - 1]
+        mon = ws.apply_rotations_and_update(k - 1)
+        rep.inner.append((restart, k - 1, mon))
+        steps = k
+        if beta < cfg.breakdown_scale * beta_cycle:
+            lucky = True
+            break
+        if not cfg.fixed_iterations and mon <= cfg.rel_tol * rep.beta0:
+            break
+        if k == m:
+            break
+        q = (u - a @ Q[:k]) / beta
+        Q[k] = q
+        # A M^-1 q_k = (w - Q_{k+1} H[:k+1, :k] a) / beta
+        Ha = ws.h_orig[: k + 1, :k] @ a
+        qw = (gamma - float(a @ b)) / beta
+        h1 = np.empty(k + 1)
+        h1[:k] = (b - Ha[:k]) / beta
+        h1[k] = (qw - Ha[k]) / beta
+        wk = (w - Ha @ Q[: k + 1]) / beta
+        u = wk - h1 @ Q[: k + 1]
+        ws.h_orig[: k + 1, k] = h1
+    return steps, lucky
+
+
 def gmres_restarted(opA, opM, b, x, cfg: GmresConfig, hook=None, orth="mgs"):
     """Right-preconditioned restarted GMRES (gmres.cpp:132-218).  x is updated."""
     n = b.size
@@ -198,7 +260,9 @@ def gmres_restarted(opA, opM, b, x, cfg: GmresConfig, hook=None, orth="mgs"):
     for restart in range(cfg.max_restarts):
         ws.begin_cycle(r, beta)
         steps, lucky = 0, False
-        for k in range(cfg.m):
+        if orth == "dcgs2":
+            steps, lucky = _dcgs2_cycle(ws, opA, opM, cfg, rep, restart, beta)
+        for k in range(cfg.m if orth != "dcgs2" else 0):
             h = ws.arnoldi_step(opA, opM, k)
             if not math.isfinite(h):
                 raise GmresError(f"gmres: non-finite Arnoldi coefficient at restart "
