@@ -157,14 +157,18 @@ def step_spmv_bytes(n, nnz, k, r):
     return 12 * nnz + 4 * (n + 1) + 16 * n + 8 * n * (k + 1) + 8 * n * r
 
 
-def class_bytes(cls, n, nnz, k, r, steps):
+def class_bytes(cls, n, nnz, k, r, steps, dcgs2=True):
     spmv = 12 * nnz + 4 * (n + 1) + 16 * n
     if cls == 0:
+        if dcgs2:  # DCGS2 step SpMV: epilogue reads W_0..W_{k-1} (both dot families), u, U, AU
+            return spmv + 8 * n * (max(k, 1) + 1 + 2 * r)
         return step_spmv_bytes(n, nnz, k, r)
-    if cls == 1:  # pass B: w1 = w - V h1 (read V_0..k, w, U_0..r-1; write w); V^T w1, ||w1||, U^T w1
+    if cls == 1:  # CGS2 pass B: w1 = w - V h1 (read V_0..k, w, U_0..r-1; write w); V^T w1, ||w1||, U^T w1
         return 8 * n * (k + 3 + r)
-    if cls == 2:  # pass C: w2 = w1 - V h2 (read V_0..k, w1; write w2), no reduction
-        return 8 * n * (k + 3)
+    if cls == 2:
+        if dcgs2:  # DCGS2 update: read W_0..W_{k-1}, u_k, y; write q_k, u_{k+1}
+            return 8 * n * (k + 4)
+        return 8 * n * (k + 3)  # CGS2 pass C: w2 = w1 - V h2
     if cls == 3:  # x += V y + U c
         return 8 * n * (steps + r + 2)
     if cls == 8:  # r = b - A x, ||r||, U^T r
@@ -273,12 +277,15 @@ def run_gpu(a):
         if c in (0, 1, 2) and (y not in steps_of or k >= steps_of[y]):
             continue  # early-exit launch after the cycle stopped
         rr = rank_of.get(y, 0)
-        b = class_bytes(c, n, nnz_local, k, rr, steps_of.get(y, a.m))
+        b = class_bytes(c, n, nnz_local, k, rr, steps_of.get(y, a.m),
+                        os.environ.get("PGMRES_DCGS2", "1") != "0")
         e = per.setdefault(c, [0.0, 0.0, 0])
         e[0] += b
         e[1] += t_ms / 1e3
         e[2] += 1
-    names = {0: "step_spmv", 1: "cgs2_passB_update_dots", 2: "cgs2_passC_update", 3: "x_update",
+    dc = os.environ.get("PGMRES_DCGS2", "1") != "0"
+    names = {0: "step_spmv", 1: "cgs2_passB_update_dots",
+             2: "dcgs2_update" if dc else "cgs2_passC_update", 3: "x_update",
              4: "ritz", 5: "push_sweeps", 6: "push_spmv", 7: "rotate", 8: "residual_spmv",
              9: "other"}
     prof_total = float(ms.sum()) / 1e3
@@ -293,8 +300,9 @@ def run_gpu(a):
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp) and a.m == 50 and world == 1:
         with open(tp) as f:
-            traffic = json.load(f).get(f"n_e={a.ne}", {}).get("k_spmv<StepEpi>", {}).get(
-                "dram_bytes_per_launch")
+            traffic = json.load(f).get(f"n_e={a.ne}", {}).get(
+                "k_spmv<DStepEpi>" if os.environ.get("PGMRES_DCGS2", "1") != "0"
+                else "k_spmv<StepEpi>", {}).get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "frac_dram": (round(traffic / (sp[1] / max(1, sp[2])) / 1e9 / peak, 4)
@@ -302,7 +310,9 @@ def run_gpu(a):
                 "note": "achieved/frac use SURVEY 8(d) algorithmic bytes (12 B per nonzero); "
                         "the kernel stores 16-bit column deltas (10 B), so frac_dram "
                         "(ncu-measured DRAM bytes / launch time) is the physical fraction",
-                "kernel": "k_spmv<StepEpi> (SpMV + AU c deflation + CGS2 pass-1 dots)",
+                "kernel": ("k_spmv<DStepEpi> (SpMV + AU c deflation + the DCGS2 step's dots)"
+                           if dc else
+                           "k_spmv<StepEpi> (SpMV + AU c deflation + CGS2 pass-1 dots)"),
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "bytes_per_launch_avg": int(sp[0] / max(1, sp[2])),
                 "launch_ms_avg": round(1e3 * sp[1] / max(1, sp[2]), 4)}

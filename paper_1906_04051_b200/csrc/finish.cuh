@@ -239,6 +239,187 @@ __device__ void fin_sweep_b(const Params& P, int k, const double* red) {
   }
 }
 
+
+// ---- DCGS2 (delayed CGS2, one reduction per Arnoldi step) ---------------------
+// Step k runs the operator on the lagged vector u_k = W_k (orthogonalised once
+// against v_0..v_{k-1}); the SpMV epilogue's ONE reduction delivers
+//   red = [W_l . y (nb), W_l . u (k), u.u, u.y, U_j . y (r)],  nb = max(k, 1).
+// The finisher completes column k-1 of H (second-pass coefficients a, the
+// subdiagonal beta = |u - Q a|), applies its Givens rotation and the exits,
+// then forms the first pass of column k through A M^-1 Q = Q H and the
+// coefficients of the single update pass (k_dcgs2_update).  Restatement:
+// oracle/pgmres_oracle.py::_dcgs2_cycle (reference parity measured there).
+// Coefficient slots: coefA[l] = -a_l s_l (l < k), coefA[k] = 1/beta;
+// coefB[l] = -(Ha_l/beta + h1_l) s_l (l < k), coefB[k] = -(Ha_k/beta + h1_k) s_k.
+// tU[k] holds U^T u_k (raw) until the step finalises it.
+
+// Column k-1 completion (thread 0; sa = a from smem).  Returns 1 to continue.
+__device__ int dcgs2_column(const Params& P, int k, const double* sa, double alpha, bool close,
+                            double* sH, double* s_beta) {
+  GState* g = P.g;
+  const int m = P.m;
+  const size_t col = (size_t)(k - 1) * (m + 1);
+  double na2 = 0.0;
+  for (int l = 0; l < k; ++l) na2 += sa[l] * sa[l];
+  const double beta = sqrt(fmax(alpha - na2, 0.0));
+  *s_beta = beta;
+  for (int l = 0; l < k; ++l) {
+    const double h = P.h_orig[col + l] + sa[l];
+    P.h_orig[col + l] = h;
+    sH[l] = h;
+  }
+  sH[k] = beta;
+  P.h_orig[col + k] = beta;
+  if (!isfinite(beta) || !isfinite(alpha)) {
+    set_error(P, 2, g->restart, k - 1);
+    return 0;
+  }
+  const int kk = k - 1;  // the column being completed
+  for (int i = 0; i < kk; ++i) {
+    const double hi = sH[i], hj = sH[i + 1];
+    sH[i] = P.cs[i] * hi + P.sn[i] * hj;
+    sH[i + 1] = -P.sn[i] * hi + P.cs[i] * hj;
+  }
+  const double a = sH[kk], b = sH[kk + 1];
+  const double rr = hypot(a, b);
+  double ck, sk;
+  if (rr == 0.0) {
+    ck = 1.0;
+    sk = 0.0;
+  } else {
+    ck = a / rr;
+    sk = b / rr;
+  }
+  P.cs[kk] = ck;
+  P.sn[kk] = sk;
+  sH[kk] = rr;
+  sH[kk + 1] = 0.0;
+  for (int i = 0; i <= kk + 1; ++i) P.h_rot[col + i] = sH[i];
+  const double gk = P.gv[kk];
+  P.gv[kk + 1] = -sk * gk;
+  P.gv[kk] = ck * gk;
+  const double monitored = fabs(-sk * gk);
+  const int idx = g->n_inner++;
+  P.rec_restart[idx] = (uint32_t)g->restart;
+  P.rec_step[idx] = (uint32_t)kk;
+  P.rec_mon[idx] = monitored;
+  g->steps = kk + 1;
+  bool stop = close || kk + 1 >= m;
+  if (beta < g->breakdown_scale * g->beta_cycle) {
+    g->lucky = 1;
+    stop = true;
+  } else if (!g->fixed && monitored <= g->rel_tol * g->beta0) {
+    stop = true;
+  }
+  if (stop) {
+    g->active = 0;
+    return 0;
+  }
+  P.s[k] = 1.0 / beta;
+  return 1;
+}
+
+__device__ void fin_dcgs2(const Params& P, int k, const double* red) {
+  __shared__ double sa[MAX_M + 1], sb[MAX_M + 1], sHa[MAX_M + 2], sh1[MAX_M + 2];
+  __shared__ double sH[MAX_M + 2];
+  __shared__ double s_beta, s_qw;
+  __shared__ int s_go;
+  const int m = P.m, R1 = P.R1, r = P.d->r;
+  const int nb = k > 0 ? k : 1;
+  const double alpha = red[nb + k], gamma = red[nb + k + 1];
+  const double* Uy = red + nb + k + 2;
+  for (int l = threadIdx.x; l < nb; l += blockDim.x) {
+    const double sl = P.s[l];
+    sb[l] = sl * red[l];
+    if (l < k) sa[l] = sl * red[nb + l];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (k == 0) {
+      s_go = 1;
+      s_beta = 1.0;
+    } else {
+      s_go = dcgs2_column(P, k, sa, alpha, false, sH, (double*)&s_beta);
+    }
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const double beta = s_beta;
+  const double ib = 1.0 / beta;
+  if (k == 0) {
+    // q_0 is final: column 0's first pass h1_0 = v_0 . y; u_1 = y - h1_0 v_0
+    if (threadIdx.x == 0) {
+      const double h1 = sb[0];
+      P.h_orig[0] = h1;
+      P.coefA[0] = 1.0;                 // 1/beta (y is not rescaled)
+      P.coefB[0] = -h1 * P.s[0];
+      P.s[1] = 1.0;
+      sh1[0] = h1;
+    }
+    __syncthreads();
+    double* tn = P.tU + (size_t)1 * R1;
+    for (int j = threadIdx.x; j < r; j += blockDim.x) tn[j] = Uy[j] - sh1[0] * P.tU[j];
+    __syncthreads();
+    defl_coeffs_par(P, r, tn, P.c);
+    return;
+  }
+  // H[:k+1, :k] a (Hessenberg: row l has columns >= l-1)
+  for (int l = threadIdx.x; l <= k; l += blockDim.x) {
+    double s = 0.0;
+    for (int j = (l > 0 ? l - 1 : 0); j < k; ++j) s += P.h_orig[(size_t)j * (m + 1) + l] * sa[j];
+    sHa[l] = s;
+  }
+  if (threadIdx.x == 0) {
+    double ab = 0.0;
+    for (int l = 0; l < k; ++l) ab += sa[l] * sb[l];
+    s_qw = (gamma - ab) * ib;  // q_k . y
+  }
+  __syncthreads();
+  const double sk = P.s[k];
+  const size_t colk = (size_t)k * (m + 1);
+  for (int l = threadIdx.x; l <= k; l += blockDim.x) {
+    const double h1 = l < k ? (sb[l] - sHa[l]) * ib : (s_qw - sHa[k]) * ib;
+    sh1[l] = h1;
+    P.h_orig[colk + l] = h1;  // first pass of column k (second pass added at step k+1)
+    if (l < k) {
+      const double sl = P.s[l];
+      P.coefA[l] = -sa[l] * sl;
+      P.coefB[l] = -(sHa[l] * ib + h1) * sl;
+    } else {
+      P.coefA[k] = ib;
+      P.coefB[k] = -(sHa[k] * ib + h1) * sk;
+    }
+  }
+  __syncthreads();
+  // U^T v_k = s_k (U^T u_k - sum_l a_l U^T v_l); U^T u_{k+1} (raw) for the next apply
+  double* tk = P.tU + (size_t)k * R1;
+  double* tn = P.tU + (size_t)(k + 1) * R1;
+  for (int j = threadIdx.x; j < r; j += blockDim.x) {
+    double t = tk[j];
+    for (int l = 0; l < k; ++l) t -= sa[l] * P.tU[(size_t)l * R1 + j];
+    const double tq = sk * t;
+    tk[j] = tq;
+    double u = Uy[j] * ib;
+    for (int l = 0; l < k; ++l) u -= (sHa[l] * ib + sh1[l]) * P.tU[(size_t)l * R1 + j];
+    u -= (sHa[k] * ib + sh1[k]) * tq;
+    tn[j] = u;
+  }
+  if (threadIdx.x == 0) P.s[k + 1] = 1.0;
+  __syncthreads();
+  defl_coeffs_par(P, r, tn, P.c);
+}
+
+// Cycle end without an early exit: red = [W_l . u_m (m), u_m . u_m] completes column m-1.
+__device__ void fin_dcgs2_close(const Params& P, const double* red) {
+  __shared__ double sa[MAX_M + 1], sH[MAX_M + 2];
+  __shared__ double s_beta;
+  const int m = P.m;
+  for (int l = threadIdx.x; l < m; l += blockDim.x) sa[l] = P.s[l] * red[l];
+  __syncthreads();
+  if (threadIdx.x == 0) dcgs2_column(P, m, sa, red[m], true, sH, (double*)&s_beta);
+  __syncthreads();
+}
+
 // ---- restart harvest: push_vector (deflation.cpp:123-184) ----------------------
 
 // red[0] = ||u||^2, red[1+l] = U_l . u

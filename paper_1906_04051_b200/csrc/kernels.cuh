@@ -269,6 +269,22 @@ struct StepEpi {
   __device__ void finish(const Params& P, const double* red) const { fin_step_spmv(P, k, red); }
 };
 
+// DCGS2 step k: y = s_k A W_k + AU c (W_k = lagged u_k for k >= 1, s_k = 1),
+// stored as W_{k+1}; ONE reduction: [W_l . y (nb), W_l . u (k), u.u, u.y,
+// U_j . y (r)], nb = max(k, 1) (finish.cuh fin_dcgs2).
+struct DStepEpi {
+  int k;
+  __device__ bool skip(const Params& P) const { return !P.g->active; }
+  __device__ int nvals(const Params& P) const { return (k > 0 ? k : 1) + k + 2 + P.d->r; }
+  __device__ void prologue(const Params& P, double* sm) const {
+    if (threadIdx.x == 0) sm[0] = P.s[k];
+    for (int l = threadIdx.x; l < P.d->r; l += blockDim.x) sm[1 + l] = P.c[l];
+  }
+  __device__ void chunk(const Params&, int, bool, double, double*, double (&)[NVL],
+                        const double*) const {}
+  __device__ void finish(const Params& P, const double* red) const { fin_dcgs2(P, k, red); }
+};
+
 // Explicit residual r = b - A x into W_0; dots ||r||^2 and U_l . r.
 struct ResidualEpi {
   int initial;
@@ -340,6 +356,10 @@ __device__ __forceinline__ const double* epi_input(const Params& P, const StepEp
   return P.V + (size_t)E.k * P.ld;
 }
 template <>
+__device__ __forceinline__ const double* epi_input(const Params& P, const DStepEpi& E) {
+  return P.V + (size_t)E.k * P.ld;
+}
+template <>
 __device__ __forceinline__ const double* epi_input(const Params& P, const ResidualEpi&) {
   return P.x;
 }
@@ -379,7 +399,9 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
   // A step SpMV of a cycle that already stopped exits before touching the
   // matrix: g->active is written by pass B's finisher, >= 2 kernels back
   // (common.cuh PDL rule), so it is final here.
-  if (std::is_same<Epi, StepEpi>::value && !*(volatile const int*)&P.g->active) return;
+  if ((std::is_same<Epi, StepEpi>::value || std::is_same<Epi, DStepEpi>::value) &&
+      !*(volatile const int*)&P.g->active)
+    return;
 #if PGM_SPMV_PREFETCH && PGM_SPMV_EARLY_PF
   {
     // L2 prefetch of this warp's first slice (values + column ids).  The
@@ -406,10 +428,11 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
   double* small = sm;
   double* ys = sm + EPI_SMALL;
   // the step epilogue needs no transpose tiles: [small | ys | bvals | red]
-  constexpr bool STEP = std::is_same<Epi, StepEpi>::value;
+  constexpr bool STEP = std::is_same<Epi, StepEpi>::value || std::is_same<Epi, DStepEpi>::value;
   double* tp = ys + TILE + (threadIdx.x >> 5) * TP_DOUBLES;
   double* wacc = ys + TILE + SPMV_WARPS * TP_DOUBLES;
-  double* bvals = STEP ? ys + TILE : wacc + SPMV_WARPS * NVL * TPR;
+  double* bvals = STEP ? ys + TILE * (std::is_same<Epi, DStepEpi>::value ? 2 : 1)
+                      : wacc + SPMV_WARPS * NVL * TPR;
   double* red = bvals + nv;
   E.prologue(P, small);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -418,6 +441,96 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
   // only live after the SpMV part, which keeps the SpMV loop's registers low
   spmv_tile<C16>(A, x, tile, ys);
   __syncthreads();
+  if constexpr (std::is_same<Epi, DStepEpi>::value) {
+    // (1) y per row -> W_{k+1}, ys; u = W_k rows -> us.  (2) one stream over
+    // each W_l (l < k) gives both W_l . y and W_l . u; U_j . y; u.u and u.y
+    // from smem.  Warp w owns vectors w, w + 8, ...
+    const int k = E.k;
+    const int r = P.d->r;
+    const size_t ld = P.ld;
+    const int row0 = tile * TILE;
+    const int rows = min(TILE, A.n - row0);
+    double* us = ys + TILE;
+    double* wnext = P.V + (size_t)(k + 1) * ld + P.lo + row0;
+    const double* uk = P.V + (size_t)k * ld + P.lo + row0;
+    const double* au0 = P.AU + P.lo + row0;
+    for (int i = threadIdx.x; i < TILE; i += SPMV_THREADS) {
+      double y = 0.0, u = 0.0;
+      if (i < rows) {
+        y = small[0] * ys[i];
+        for (int l = 0; l < r; ++l) y += small[1 + l] * __ldg(au0 + (size_t)l * ld + i);
+        wnext[i] = y;
+        u = uk[i];
+      }
+      ys[i] = y;
+      us[i] = u;
+    }
+    __syncthreads();
+    const int nb = k > 0 ? k : 1;
+    const double* v0 = P.V + P.lo + row0;
+    const int nvec = nb + r + 1;  // W_l (l < nb), U_j, and one slot for u.u / u.y
+    for (int q = warp; q < nvec; q += SPMV_WARPS) {
+      double ay = 0.0, au = 0.0;
+      if (q < nb) {
+        const double* v = v0 + (size_t)q * ld + lane;
+        if (rows == TILE) {  // full tile: all 16 loads in flight, then the products
+          double t[TILE / 32];
+#pragma unroll
+          for (int i = 0; i < TILE / 32; ++i) t[i] = __ldg(v + 32 * i);
+#pragma unroll
+          for (int i = 0; i < TILE / 32; ++i) {
+            ay += t[i] * ys[lane + 32 * i];
+            au += t[i] * us[lane + 32 * i];
+          }
+        } else {
+          for (int t = 0; t < TILE / 32; ++t) {
+            if (lane + 32 * t < rows) {
+              const double w = __ldg(v + 32 * t);
+              ay += w * ys[lane + 32 * t];
+              au += w * us[lane + 32 * t];
+            }
+          }
+        }
+        ay = warp_sum(ay);
+        au = warp_sum(au);
+        if (lane == 0) {
+          bvals[q] = ay;
+          if (q < k) bvals[nb + q] = au;
+        }
+      } else if (q < nb + r) {
+        const double* v = P.U + (size_t)(q - nb) * ld + P.lo + row0 + lane;
+        if (rows == TILE) {
+          double t[TILE / 32];
+#pragma unroll
+          for (int i = 0; i < TILE / 32; ++i) t[i] = __ldg(v + 32 * i);
+#pragma unroll
+          for (int i = 0; i < TILE / 32; ++i) ay += t[i] * ys[lane + 32 * i];
+        } else {
+          for (int t = 0; t < TILE / 32; ++t)
+            if (lane + 32 * t < rows) ay += __ldg(v + 32 * t) * ys[lane + 32 * t];
+        }
+        ay = warp_sum(ay);
+        if (lane == 0) bvals[nb + k + 2 + (q - nb)] = ay;
+      } else {
+        for (int t = 0; t < TILE / 32; ++t) {
+          const double u = us[lane + 32 * t];
+          ay += u * u;
+          au += u * ys[lane + 32 * t];
+        }
+        ay = warp_sum(ay);
+        au = warp_sum(au);
+        if (lane == 0) {
+          bvals[nb + k] = ay;
+          bvals[nb + k + 1] = au;
+        }
+      }
+    }
+    pdl_trigger();
+    __syncthreads();
+    const int G = SEG ? A.ntiles : (int)gridDim.x;
+    if (reduce_tail(bvals, nv, P, red, G, tile)) E.finish(P, red);
+    return;
+  }
   if constexpr (std::is_same<Epi, StepEpi>::value) {
     // Step epilogue, two phases.  (1) y = s_k (A W_k) + AU c -> W_{k+1} and
     // ys, thread per row.  (2) pass-1 dots W_l . y: warp w owns the basis
@@ -553,6 +666,7 @@ enum SweepMode {
   SW_PUSH3 = 5,    // u -= U proj ; ||u||^2
   SW_DOTS_U = 6,   // U^T u only (apply)
   SW_AXPY_U = 7,   // u += U c only (apply)
+  SW_DCLOSE = 8,   // DCGS2 cycle close: W_l . u_m, ||u_m||^2
 };
 
 struct SweepSpec {
@@ -588,6 +702,13 @@ __device__ __forceinline__ SweepSpec sweep_spec(const Params& P, int k) {
     S.Q = S.Pv;
     S.nq = k + 1;
     S.qstaged = 1;
+    S.selfnorm = 1;
+    S.normlast = 1;
+  } else if (MODE == SW_DCLOSE) {
+    S.skip = !g->active;
+    S.in = S.out = P.V + (size_t)P.m * P.ld + lo;
+    S.Q = P.V + lo;
+    S.nq = P.m;
     S.selfnorm = 1;
     S.normlast = 1;
   } else if (MODE == SW_XUPDATE) {
@@ -651,6 +772,7 @@ __device__ __forceinline__ void sweep_finish(const Params& P, int k, const doubl
   if (MODE == SW_PUSH1 && threadIdx.x == 0) fin_push1(P, red);
   if (MODE == SW_PUSH2 && threadIdx.x == 0) fin_push2(P, red);
   if (MODE == SW_PUSH3 && threadIdx.x == 0) fin_push3(P, red);
+  if (MODE == SW_DCLOSE) fin_dcgs2_close(P, red);
   if (MODE == SW_DOTS_U) {
     for (int l = threadIdx.x; l < P.d->r; l += blockDim.x) P.proj[l] = red[l];
     __syncthreads();
@@ -1008,6 +1130,57 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_cgs2_update(Params P, int k) {
   pdl_trigger();
 }
 
+// DCGS2 update pass (one stream over W_0..W_{k-1}, u_k = W_k, y = W_{k+1}):
+//   q_k (unnormalised)  W_k     = u + sum_{l<k} coefA_l W_l          (k >= 1)
+//   u_{k+1}             W_{k+1} = coefA_k y + sum_{l<k} coefB_l W_l + coefB_k W_k'
+__global__ void __launch_bounds__(UPD_BLOCK) k_dcgs2_update(Params P, int k) {
+  __shared__ double ca[MAX_M + 8], cb[MAX_M + 8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = P.n;
+  const size_t ld = P.ld;
+  const int nch = (n + 63) >> 6;
+  const int W = gridDim.x * (UPD_BLOCK / 32);
+  const double* V0 = P.V + P.lo;
+  pdl_wait();
+  if (!P.g->active) return;
+  for (int l = threadIdx.x; l < k + 8; l += UPD_BLOCK) {
+    ca[l] = l <= k ? P.coefA[l] : 0.0;
+    cb[l] = l <= k ? P.coefB[l] : 0.0;
+  }
+  __syncthreads();
+  double* wk = P.V + (size_t)k * ld + P.lo;
+  double* wn = P.V + (size_t)(k + 1) * ld + P.lo;
+  for (int c = blockIdx.x * (UPD_BLOCK / 32) + warp; c < nch; c += W) {
+    const int row0 = c * 64 + 2 * lane;
+    double2 q = *reinterpret_cast<const double2*>(wk + row0);
+    const double2 y = *reinterpret_cast<const double2*>(wn + row0);
+    double2 un = make_double2(0.0, 0.0);
+    for (int l0 = 0; l0 < k; l0 += 8) {
+      double2 t[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        t[j] = (l0 + j < k) ? __ldg(reinterpret_cast<const double2*>(V0 + (size_t)(l0 + j) * ld + row0))
+                            : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        q.x += ca[l0 + j] * t[j].x;
+        q.y += ca[l0 + j] * t[j].y;
+        un.x += cb[l0 + j] * t[j].x;
+        un.y += cb[l0 + j] * t[j].y;
+      }
+    }
+    const double2 o = make_double2(ca[k] * y.x + un.x + cb[k] * q.x, ca[k] * y.y + un.y + cb[k] * q.y);
+    if (row0 + 1 < n) {
+      if (k > 0) *reinterpret_cast<double2*>(wk + row0) = q;
+      *reinterpret_cast<double2*>(wn + row0) = o;
+    } else if (row0 < n) {
+      if (k > 0) wk[row0] = q.x;
+      wn[row0] = o.x;
+    }
+  }
+  pdl_trigger();
+}
+
 // Cross-GPU path: finisher after the allreduce of P.red_out.
 template <int KIND>
 __global__ void k_finish(Params P, int k) {
@@ -1020,6 +1193,8 @@ __global__ void k_finish(Params P, int k) {
     if (!(P.g->error != 0 || (!k && P.g->done))) fin_residual(P, red, k != 0);
   } else if (KIND == 102) {
     if (P.d->push_ok && threadIdx.x == 0) fin_push_spmv(P, red);
+  } else if (KIND == 103) {
+    if (P.g->active) fin_dcgs2(P, k, red);
   } else {
     const SweepSpec S = sweep_spec<KIND>(P, k);
     if (!S.skip) sweep_finish<KIND>(P, k, red);

@@ -177,6 +177,8 @@ struct pgm_context {
   // optional per-launch profiling (CUDA events around every hot-path kernel)
   bool prof_on = false;
   bool pdl = true;  // programmatic dependent launch of the hot-path kernels (PGMRES_PDL=0 disables)
+  bool dcgs2 = true;  // delayed CGS2, one reduction per Arnoldi step (PGMRES_DCGS2=0: CGS2)
+  bool dc_now = true;  // this solve runs DCGS2
   int prof_cycle = 0;
   struct Rec {
     uint32_t cls, cyc, k;
@@ -317,6 +319,10 @@ uint32_t prof_class_of<StepEpi>() {
   return PC_STEP_SPMV;
 }
 template <>
+uint32_t prof_class_of<DStepEpi>() {
+  return PC_STEP_SPMV;
+}
+template <>
 uint32_t prof_class_of<ResidualEpi>() {
   return PC_RESIDUAL;
 }
@@ -351,7 +357,9 @@ Status launch_spmv(pgm_context* ctx, const pgm_matrix* A, const Params& P, const
                    int nvmax, uint32_t prof_k = 0, int seg = 0) {
   const size_t smem = std::is_same<Epi, StepEpi>::value
                           ? sizeof(double) * spmv_step_smem_doubles(nvmax)
-                          : spmv_smem(nvmax);
+                          : std::is_same<Epi, DStepEpi>::value
+                                ? sizeof(double) * (spmv_step_smem_doubles(nvmax) + TILE)
+                                : spmv_smem(nvmax);
   Sell sv = A->view();
   SpmvSeg sg{0, 0, 0};
   int G = std::max(1, A->ntiles);
@@ -366,7 +374,7 @@ Status launch_spmv(pgm_context* ctx, const pgm_matrix* A, const Params& P, const
   ProfScope ps(ctx, prof_class_of<Epi>(), prof_k);
   // one tile per block: the hardware scheduler balances the tiles
   const bool c16 = A->col16 != nullptr;
-  if constexpr (std::is_same<Epi, StepEpi>::value) {
+  if constexpr (std::is_same<Epi, StepEpi>::value || std::is_same<Epi, DStepEpi>::value) {
     if (seg != 0) {
       const Status st = c16 ? launch_spmv_k<Epi, true, true>(ctx, G, smem, sv, P, E, sg)
                             : launch_spmv_k<Epi, true, false>(ctx, G, smem, sv, P, E, sg);
@@ -426,6 +434,19 @@ constexpr int CGS2_SPLIT_MAX = 112;  // = MAX_M: 8 warps x 14 vectors
 #ifndef PGM_CGS2_RPL
 #define PGM_CGS2_RPL 2  // rows per lane (tools/run_variants.sh study: 2 beats 1)
 #endif
+Status launch_dcgs2_update(pgm_context* ctx, const Params& P, int k) {
+  static int occ = 0;
+  if (occ == 0) occ = std::min(MAX_BLOCKS_PER_SM, occupancy(k_dcgs2_update, UPD_BLOCK, 0));
+  const int nchunks = (int)((ctx->n + 63) / 64);
+  const int G = std::max(1, std::min((nchunks + UPD_BLOCK / 32 - 1) / (UPD_BLOCK / 32),
+                                     occ * ctx->nsm));
+  ProfScope ps(ctx, PC_SWEEP_C, (uint32_t)k);
+  CU(launch_pdl(ctx, k_dcgs2_update, G, UPD_BLOCK, 0, P, k));
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return {};
+}
+
 Status launch_cgs2_update(pgm_context* ctx, const Params& P, int k) {
   static int occ = 0;
   if (occ == 0) occ = std::min(MAX_BLOCKS_PER_SM, occupancy(k_cgs2_update, UPD_BLOCK, 0));
@@ -739,7 +760,20 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
   const int m = ctx->ws_m;
   const int R1 = d->R1;
   const bool overlap = ctx->world > 1 && A->t_hi_begin > A->t_lo_end;
-  for (int k = 0; k < m; ++k) {
+  if (ctx->dc_now) {
+    // delayed CGS2: SpMV (+ the step's one reduction) and one update per step,
+    // the cycle closes with a dots-only pass for column m-1
+    for (int k = 0; k < m; ++k) {
+      if (ctx->world > 1) TRY(halo_exchange(ctx, HV_V, k));
+      DStepEpi se{k};
+      TRY(launch_spmv(ctx, A, P, se, 2 * m + 2 + R1, (uint32_t)k));
+      TRY(finish_global<103>(ctx, P, k, std::max(k, 1) + k + 2 + R1));
+      TRY(launch_dcgs2_update(ctx, P, k));
+    }
+    TRY(launch_sweep<SW_DCLOSE>(ctx, P, m, 0, 0, m + 1, false));
+    TRY(finish_global<SW_DCLOSE>(ctx, P, m, m + 1));
+  }
+  for (int k = 0; k < (ctx->dc_now ? 0 : m); ++k) {
     if (overlap) {
       // halo planes of W_k on hstream (NVLink P2P through NCCL send/recv)
       // while the interior tiles run; then the boundary tiles.  NCCL calls
@@ -868,7 +902,11 @@ Status solve_impl(pgm_context* ctx, pgm_matrix* A, pgm_deflator* dflt, const dou
   if (d->ctx != ctx) return einval("pgm_solve: deflator belongs to another context");
   const int m = (int)cfg->m;
   const int maxr = (int)cfg->max_restarts;
-  TRY(ensure_reduction(ctx, std::max(m + 1, 2 * d->R1 + 1), A->ntiles));
+  TRY(ensure_reduction(ctx, std::max(std::max(m + 1, 2 * d->R1 + 1), 2 * m + 2 + d->R1),
+                       A->ntiles));
+  // the peer window slot bounds the DCGS2 reduction (2m + 2 + r values):
+  // larger restart lengths use CGS2 on the peer transport
+  ctx->dc_now = ctx->dcgs2 && !(ctx->peer && 2 * m + 2 + d->R1 > PEER_NV);
   TRY(ensure_workspace(ctx, m, maxr, std::max(d->R1, 1)));
   TRY(defl_alloc_vectors(d));
   if (harvest) {
@@ -1201,6 +1239,7 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) 
   }
   auto* ctx = new pgm_context();
   if (const char* e = std::getenv("PGMRES_PDL")) ctx->pdl = e[0] != '0';
+  if (const char* e = std::getenv("PGMRES_DCGS2")) ctx->dcgs2 = e[0] != '0';
   ctx->device = cfg->device;
   ctx->rank = cfg->rank;
   ctx->world = cfg->world;

@@ -497,3 +497,25 @@ def test_restart_length_sweep_ne25(torch_cuda, golden, m, defl):
     assert abs(np.linalg.norm(xh) - float(g[key + "_x_norm"])) <= X_TOL * float(g[key + "_x_norm"])
     assert np.linalg.norm(xh[::97] - g[key + "_x_sample"]) <= 10 * X_TOL * np.linalg.norm(
         g[key + "_x_sample"])
+
+
+@pytest.mark.parametrize("variant", ["cgs2"])
+def test_cgs2_path_still_matches(torch_cuda, ref, golden, monkeypatch, variant):
+    """PGMRES_DCGS2=0 keeps the two-reduction CGS2 step (pass B + pass C) —
+    the DCGS2 default's fallback (peer transport with a large restart length)."""
+    monkeypatch.setenv("PGMRES_DCGS2", "0")
+    A, _, b = _csr(ref, 10)
+    g = golden("cfg1_defl")
+    ex = pg.DeviceExecutor()
+    d = pg.Deflator()
+    x = np.zeros(A.n)
+    rep = pg.deflated_gmres(A, b, x, pg.GmresConfig(m=30, rel_tol=1e-10), d, ex)
+    assert rep.restarts == int(g["restarts"])
+    _compare(rep, g, x, g["x"])
+    gt = golden("ne10_m4_trunc")
+    A2, _, b2 = _csr(ref, 10)
+    d2 = pg.Deflator()
+    x2 = np.zeros(A2.n)
+    pg.deflated_gmres(A2, b2, x2, pg.GmresConfig(m=4, max_restarts=24, fixed_iterations=True), d2,
+                      pg.DeviceExecutor())
+    assert [h.r for h in d2.history()] == list(gt["hist_r"])

@@ -8,5 +8,6 @@ for d in paper_1906_04051_b200/_lib/var/*/; do
 import json
 d=json.load(open('gpurun_out/var_$name.json'))
 k=d['kernels']
-print('%-10s %8.1f it/s %7.2f ms  spmv %6.2f  B %6.2f  C %6.2f' % ('$name', d['value'], d['ms_per_step'], k['step_spmv']['ms_total'], k['cgs2_passB_update_dots']['ms_total'], k['cgs2_passC_update']['ms_total']))"
+g=lambda n: k.get(n, {}).get('ms_total', 0.0)
+print('%-10s %8.1f it/s %7.2f ms  spmv %6.2f  B %6.2f  C/update %6.2f' % ('$name', d['value'], d['ms_per_step'], g('step_spmv'), g('cgs2_passB_update_dots'), g('cgs2_passC_update') + g('dcgs2_update')))"
 done
