@@ -1130,6 +1130,9 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_cgs2_update(Params P, int k) {
   pdl_trigger();
 }
 
+#ifndef PGM_DUPD_PF
+#define PGM_DUPD_PF 0
+#endif
 // DCGS2 update pass (one stream over W_0..W_{k-1}, u_k = W_k, y = W_{k+1}):
 //   q_k (unnormalised)  W_k     = u + sum_{l<k} coefA_l W_l          (k >= 1)
 //   u_{k+1}             W_{k+1} = coefA_k y + sum_{l<k} coefB_l W_l + coefB_k W_k'
@@ -1151,6 +1154,12 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_dcgs2_update(Params P, int k) {
   double* wk = P.V + (size_t)k * ld + P.lo;
   double* wn = P.V + (size_t)(k + 1) * ld + P.lo;
   for (int c = blockIdx.x * (UPD_BLOCK / 32) + warp; c < nch; c += W) {
+#if PGM_DUPD_PF
+    // L2 prefetch of this warp's next chunk: W_0..W_{k+1}, one 512 B segment per lane
+    if (c + W < nch)
+      for (int l = lane; l < k + 2; l += 32)
+        tma_prefetch_l2(V0 + (size_t)l * ld + (size_t)(c + W) * 64, 512);
+#endif
     const int row0 = c * 64 + 2 * lane;
     double2 q = *reinterpret_cast<const double2*>(wk + row0);
     const double2 y = *reinterpret_cast<const double2*>(wn + row0);

@@ -4,7 +4,7 @@
 #   bench_cfg3.json / bench_cfg2.json   python bench.py (default = cfg3) / --ne 50
 #   bench_ref_cfg3.json / _cfg2.json    python bench.py --impl reference [...]
 #   launches_ne{125,50}.txt/.json       ncu launch list (time + DRAM bytes) of one solve
-#   ncu_*.txt                           ncu --set full of the step SpMV, pass B, pass C at k = 25 (cfg3)
+#   ncu_*.txt                           ncu --set full of the step SpMV and the DCGS2 update at k = 25 (cfg3)
 set -x
 cd "$(dirname "$0")/.."
 python bench.py > gpurun_out/bench_cfg3.json 2> gpurun_out/bench_cfg3.err
@@ -22,10 +22,8 @@ done
 # SpMV is launch 0 of k_spmv)
 ncu --set full --clock-control none --import-source on -k regex:^k_spmv$ -s 26 -c 1 \
     -f -o /tmp/ncu_step_spmv python tools/profile_solve.py --ne 125 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:^k_cgs2$ -s 25 -c 1 \
-    -f -o /tmp/ncu_cgs2_b python tools/profile_solve.py --ne 125 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:^k_cgs2_update$ -s 25 -c 1 \
-    -f -o /tmp/ncu_cgs2_c python tools/profile_solve.py --ne 125 > /dev/null 2>&1
-for r in step_spmv cgs2_b cgs2_c; do
+ncu --set full --clock-control none --import-source on -k regex:^k_dcgs2_update$ -s 25 -c 1 \
+    -f -o /tmp/ncu_dcgs2_update python tools/profile_solve.py --ne 125 > /dev/null 2>&1
+for r in step_spmv dcgs2_update; do
   python tools/ncu_summary.py /tmp/ncu_$r.ncu-rep > gpurun_out/ncu_$r.txt 2>&1
 done
