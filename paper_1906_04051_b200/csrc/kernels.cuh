@@ -1133,11 +1133,14 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_cgs2_update(Params P, int k) {
 #ifndef PGM_DUPD_PF
 #define PGM_DUPD_PF 0
 #endif
+#ifndef PGM_DUPD_BATCH
+#define PGM_DUPD_BATCH 4  // basis vectors per load batch (measured: 4 and 16 beat 8)
+#endif
 // DCGS2 update pass (one stream over W_0..W_{k-1}, u_k = W_k, y = W_{k+1}):
 //   q_k (unnormalised)  W_k     = u + sum_{l<k} coefA_l W_l          (k >= 1)
 //   u_{k+1}             W_{k+1} = coefA_k y + sum_{l<k} coefB_l W_l + coefB_k W_k'
 __global__ void __launch_bounds__(UPD_BLOCK) k_dcgs2_update(Params P, int k) {
-  __shared__ double ca[MAX_M + 8], cb[MAX_M + 8];
+  __shared__ double ca[MAX_M + 32], cb[MAX_M + 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = P.n;
   const size_t ld = P.ld;
@@ -1146,7 +1149,7 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_dcgs2_update(Params P, int k) {
   const double* V0 = P.V + P.lo;
   pdl_wait();
   if (!P.g->active) return;
-  for (int l = threadIdx.x; l < k + 8; l += UPD_BLOCK) {
+  for (int l = threadIdx.x; l < k + PGM_DUPD_BATCH; l += UPD_BLOCK) {
     ca[l] = l <= k ? P.coefA[l] : 0.0;
     cb[l] = l <= k ? P.coefB[l] : 0.0;
   }
@@ -1164,14 +1167,14 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_dcgs2_update(Params P, int k) {
     double2 q = *reinterpret_cast<const double2*>(wk + row0);
     const double2 y = *reinterpret_cast<const double2*>(wn + row0);
     double2 un = make_double2(0.0, 0.0);
-    for (int l0 = 0; l0 < k; l0 += 8) {
-      double2 t[8];
+    for (int l0 = 0; l0 < k; l0 += PGM_DUPD_BATCH) {
+      double2 t[PGM_DUPD_BATCH];
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < PGM_DUPD_BATCH; ++j)
         t[j] = (l0 + j < k) ? __ldg(reinterpret_cast<const double2*>(V0 + (size_t)(l0 + j) * ld + row0))
                             : make_double2(0.0, 0.0);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < PGM_DUPD_BATCH; ++j) {
         q.x += ca[l0 + j] * t[j].x;
         q.y += ca[l0 + j] * t[j].y;
         un.x += cb[l0 + j] * t[j].x;
