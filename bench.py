@@ -16,7 +16,8 @@ n_e = 125, 15,813,251 DOF, 991,266,025 nnz (the matrix, 11.9 GB, dwarfs the
 `e2e`    : same metric through the public API with HOST buffers: full CSR
            upload + b + x0 host->device, solve, x device->host, every step.
 `roofline`: the step SpMV kernel (SpMV fused with the deflation correction and
-           the CGS2 pass-1 dots), algorithmic bytes / its CUDA-event duration.
+           the Arnoldi step's dot products), algorithmic bytes / its CUDA-event
+           duration; `traffic` / `frac_dram` from the committed ncu launch list.
 `cpu_baseline`: the reference CPU solver (oracle/_ref, the reference's own
            sources) on a bounded sample of the same system, all host cores.
 --impl reference: the reference CPU solver itself, rank 0 only (a bounded

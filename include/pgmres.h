@@ -184,7 +184,8 @@ pgm_status pgm_peer_import(pgm_context* ctx, const void* all /* world * 128 byte
 /* Kernel launches of the last pgm_solve (evidence for the bench). */
 uint64_t pgm_context_launch_count(const pgm_context* ctx);
 /* Optional CUDA-event timing of every hot-path kernel of the next solves
- * (class ids: 0 step SpMV, 1 CGS2 pass-2 dots, 2 CGS2 update+norm, 3 x update,
+ * (class ids: 0 step SpMV, 1 CGS2 pass B (CGS2 step only), 2 DCGS2 update / CGS2
+ * pass C, 3 x update,
  * 4 Ritz, 5 push sweeps, 6 push SpMV, 7 rotate, 8 residual, 9 other). */
 pgm_status pgm_context_set_profiling(pgm_context* ctx, int32_t on);
 uint32_t pgm_context_profile(pgm_context* ctx, uint32_t* cls, uint32_t* cycle, uint32_t* k,
