@@ -764,9 +764,20 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
     // delayed CGS2: SpMV (+ the step's one reduction) and one update per step,
     // the cycle closes with a dots-only pass for column m-1
     for (int k = 0; k < m; ++k) {
-      if (ctx->world > 1) TRY(halo_exchange(ctx, HV_V, k));
       DStepEpi se{k};
-      TRY(launch_spmv(ctx, A, P, se, 2 * m + 2 + R1, (uint32_t)k));
+      if (overlap) {
+        // halo planes of W_k (= u_k) on hstream while the interior tiles run
+        CU(cudaEventRecord(ctx->ev_halo_src, ctx->stream));
+        CU(cudaStreamWaitEvent(ctx->hstream, ctx->ev_halo_src, 0));
+        TRY(halo_exchange(ctx, HV_V, k, ctx->hstream));
+        CU(cudaEventRecord(ctx->ev_halo_done, ctx->hstream));
+        TRY(launch_spmv(ctx, A, P, se, 2 * m + 2 + R1, (uint32_t)k, 1));
+        CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo_done, 0));
+        TRY(launch_spmv(ctx, A, P, se, 2 * m + 2 + R1, (uint32_t)k, 2));
+      } else {
+        if (ctx->world > 1) TRY(halo_exchange(ctx, HV_V, k));
+        TRY(launch_spmv(ctx, A, P, se, 2 * m + 2 + R1, (uint32_t)k));
+      }
       TRY(finish_global<103>(ctx, P, k, std::max(k, 1) + k + 2 + R1));
       TRY(launch_dcgs2_update(ctx, P, k));
     }
