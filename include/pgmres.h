@@ -57,8 +57,9 @@ typedef struct {
   const void* nccl_id;    /* 128-byte ncclUniqueId from rank 0 (world > 1)   */
   pgm_loopback* loopback; /* instead of NCCL: in-process group of `world`    */
                           /* contexts driven by one host thread each         */
-  uint32_t n_axis;        /* node planes; plane = n_axis^2 rows (0: n/world   */
-                          /* contiguous split without mesh structure)        */
+  uint32_t n_axis;        /* node planes; plane = n_axis^2 rows.  Required   */
+                          /* when world > 1 (z-slab partition); 0 = no mesh  */
+                          /* structure, accepted for world = 1 only          */
   uint32_t n_global;      /* total rows                                      */
   int32_t deterministic;  /* reserved: reduction order is always fixed       */
 } pgm_context_config;

@@ -16,8 +16,6 @@
 namespace pgm {
 namespace dense {
 
-PGM_HD double sgn_of(double a, double b) { return b >= 0.0 ? fabs(a) : -fabs(a); }
-
 // In-place LU with partial pivoting (row interchanges recorded in perm:
 // row i of the factor is row perm[i] of the input).  Mirrors the unblocked
 // Doolittle scheme of a PartialPivLU: a zero pivot column is skipped.
@@ -81,176 +79,163 @@ PGM_HD void invert(double* a, int n, int ld, double* inv, int ld_inv, int* perm,
   }
 }
 
-// Reduce a general matrix to upper Hessenberg form by stabilised elementary
-// similarity transformations (Gaussian elimination with pivoting); entries
-// below the first subdiagonal are zeroed on return.
-PGM_HD void hessenberg(double* a, int n, int ld) {
+// Orthogonal reduction to upper Hessenberg form, A <- P^T A P with one
+// Householder reflector per column (P = P_0 ... P_{n-3}); entries below the
+// first subdiagonal are zeroed on return.
+PGM_HD void hessenberg_reduce(double* a, int n, int ld) {
 #define A_(i, j) a[(i) + (j) * ld]
-  for (int m = 1; m < n - 1; ++m) {
-    double x = 0.0;
-    int piv = m;
-    for (int j = m; j < n; ++j)
-      if (fabs(A_(j, m - 1)) > fabs(x)) {
-        x = A_(j, m - 1);
-        piv = j;
-      }
-    if (piv != m) {
-      for (int j = m - 1; j < n; ++j) {
-        const double t = A_(piv, j);
-        A_(piv, j) = A_(m, j);
-        A_(m, j) = t;
-      }
-      for (int j = 0; j < n; ++j) {
-        const double t = A_(j, piv);
-        A_(j, piv) = A_(j, m);
-        A_(j, m) = t;
-      }
+  for (int c = 0; c + 2 < n; ++c) {
+    // reflector v (stored over A(c+1:n, c)) with (I - 2 v v^T / v^T v) x = alpha e_1
+    double sq = 0.0;
+    for (int i = c + 1; i < n; ++i) sq += A_(i, c) * A_(i, c);
+    const double xnorm = sqrt(sq);
+    if (xnorm == 0.0) continue;
+    const double x0 = A_(c + 1, c);
+    const double alpha = x0 > 0.0 ? -xnorm : xnorm;
+    A_(c + 1, c) = x0 - alpha;
+    const double vtv = sq - x0 * x0 + A_(c + 1, c) * A_(c + 1, c);
+    if (vtv == 0.0) {
+      A_(c + 1, c) = x0;
+      continue;
     }
-    if (x != 0.0) {
-      for (int i = m + 1; i < n; ++i) {
-        double y = A_(i, m - 1);
-        if (y != 0.0) {
-          y /= x;
-          A_(i, m - 1) = y;
-          for (int j = m; j < n; ++j) A_(i, j) -= y * A_(m, j);
-          for (int j = 0; j < n; ++j) A_(j, m) += y * A_(j, i);
-        }
-      }
+    const double tau = 2.0 / vtv;
+    // left: rows c+1..n-1 of columns c+1..n-1
+    for (int j = c + 1; j < n; ++j) {
+      double d = 0.0;
+      for (int i = c + 1; i < n; ++i) d += A_(i, c) * A_(i, j);
+      d *= tau;
+      for (int i = c + 1; i < n; ++i) A_(i, j) -= d * A_(i, c);
     }
+    // right: columns c+1..n-1 of every row
+    for (int i = 0; i < n; ++i) {
+      double d = 0.0;
+      for (int j = c + 1; j < n; ++j) d += A_(i, j) * A_(j, c);
+      d *= tau;
+      for (int j = c + 1; j < n; ++j) A_(i, j) -= d * A_(j, c);
+    }
+    A_(c + 1, c) = alpha;
+    for (int i = c + 2; i < n; ++i) A_(i, c) = 0.0;
   }
-  for (int j = 0; j < n; ++j)
-    for (int i = j + 2; i < n; ++i) A_(i, j) = 0.0;
 #undef A_
 }
 
-// Eigenvalues of an upper Hessenberg matrix by the Francis double-shift QR
-// iteration (destroys a).  Returns false if an eigenvalue fails to converge
-// in 30 iterations.
-PGM_HD bool hqr(double* a, int n, int ld, double* wr, double* wi) {
-#define A_(i, j) a[(i) + (j) * ld]
-  double anorm = 0.0;
-  for (int i = 0; i < n; ++i)
-    for (int j = (i > 0 ? i - 1 : 0); j < n; ++j) anorm += fabs(A_(i, j));
-  int nn = n - 1;
-  double t = 0.0;
-  double p = 0.0, q = 0.0, r = 0.0, s, w, x, y, z = 0.0;
-  while (nn >= 0) {
-    int its = 0, l;
-    do {
-      for (l = nn; l >= 1; --l) {
-        s = fabs(A_(l - 1, l - 1)) + fabs(A_(l, l));
-        if (s == 0.0) s = anorm;
-        if (fabs(A_(l, l - 1)) + s == s) {
-          A_(l, l - 1) = 0.0;
-          break;
-        }
+// Minimal complex arithmetic for the shifted QR below.
+struct cplx {
+  double re, im;
+};
+PGM_HD cplx c_make(double re, double im) { return cplx{re, im}; }
+PGM_HD cplx c_add(cplx a, cplx b) { return cplx{a.re + b.re, a.im + b.im}; }
+PGM_HD cplx c_sub(cplx a, cplx b) { return cplx{a.re - b.re, a.im - b.im}; }
+PGM_HD cplx c_mul(cplx a, cplx b) {
+  return cplx{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+PGM_HD cplx c_conj(cplx a) { return cplx{a.re, -a.im}; }
+PGM_HD cplx c_scale(cplx a, double s) { return cplx{a.re * s, a.im * s}; }
+PGM_HD double c_abs(cplx a) { return hypot(a.re, a.im); }
+PGM_HD cplx c_sqrt(cplx a) {  // principal branch
+  const double r = c_abs(a);
+  if (r == 0.0) return cplx{0.0, 0.0};
+  const double t = sqrt(0.5 * (r + fabs(a.re)));
+  if (a.re >= 0.0) return cplx{t, 0.5 * a.im / t};
+  return cplx{0.5 * fabs(a.im) / t, a.im >= 0.0 ? t : -t};
+}
+
+// Eigenvalues of a real upper Hessenberg matrix `h` (not modified) by the
+// explicitly shifted QR iteration in complex arithmetic: each sweep factors
+// H - mu I = QR over the active window with complex Givens rotations
+// G = [c s; -conj(s) c] (c real) and forms RQ + mu I; mu is the eigenvalue
+// of the trailing 2x2 nearest its last diagonal entry (Wilkinson), with an
+// ad-hoc shift every 10th sweep of a window.  A subdiagonal entry below
+// eps * (|h_{i-1,i-1}| + |h_ii|) splits the window.  zwork: >= 2*n*n + n
+// doubles.  Returns false if a window needs more than 90 sweeps.
+PGM_HD bool hessenberg_eigvals(const double* h, int n, int ld, double* wr, double* wi,
+                               double* zwork) {
+  cplx* z = reinterpret_cast<cplx*>(zwork);  // n x n, column-major
+  double* gc = zwork + 2 * n * n;            // n rotation cosines
+#define Z_(i, j) z[(i) + (j) * n]
+  double fro = 0.0;
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      const double v = (i <= j + 1) ? h[i + j * ld] : 0.0;
+      Z_(i, j) = c_make(v, 0.0);
+      fro += v * v;
+    }
+  fro = sqrt(fro);
+  const double eps = 2.220446049250313e-16;
+  int hi = n - 1, sweeps = 0;
+  while (hi >= 0) {
+    int lo = hi;
+    while (lo > 0) {
+      double s = c_abs(Z_(lo - 1, lo - 1)) + c_abs(Z_(lo, lo));
+      if (s == 0.0) s = fro;
+      if (c_abs(Z_(lo, lo - 1)) <= eps * s) {
+        Z_(lo, lo - 1) = c_make(0.0, 0.0);
+        break;
       }
-      x = A_(nn, nn);
-      if (l == nn) {
-        wr[nn] = x + t;
-        wi[nn] = 0.0;
-        --nn;
+      --lo;
+    }
+    if (lo == hi) {
+      wr[hi] = Z_(hi, hi).re;
+      wi[hi] = Z_(hi, hi).im;
+      --hi;
+      sweeps = 0;
+      continue;
+    }
+    if (++sweeps > 90) return false;
+    cplx mu;
+    if (sweeps % 10 == 0) {
+      const double t = c_abs(Z_(hi, hi - 1)) + (hi >= 2 ? c_abs(Z_(hi - 1, hi - 2)) : 0.0);
+      mu = c_add(Z_(hi, hi), c_make(0.75 * t, 0.25 * t));
+    } else {
+      const cplx p = Z_(hi - 1, hi - 1), q = Z_(hi - 1, hi), r = Z_(hi, hi - 1), d = Z_(hi, hi);
+      const cplx half = c_scale(c_sub(p, d), 0.5);
+      const cplx disc = c_sqrt(c_add(c_mul(half, half), c_mul(q, r)));
+      const cplx mid = c_scale(c_add(p, d), 0.5);
+      const cplx m1 = c_add(mid, disc), m2 = c_sub(mid, disc);
+      mu = c_abs(c_sub(m1, d)) <= c_abs(c_sub(m2, d)) ? m1 : m2;
+    }
+    for (int i = lo; i <= hi; ++i) Z_(i, i) = c_sub(Z_(i, i), mu);
+    // QR: rotations k = lo..hi-1 zero Z(k+1, k); the sine of rotation k is
+    // parked in Z(k+1, k), which it zeroes
+    for (int k = lo; k < hi; ++k) {
+      const cplx x = Z_(k, k), y = Z_(k + 1, k);
+      const double ax = c_abs(x), ay = c_abs(y);
+      const double rr = hypot(ax, ay);
+      double c;
+      cplx sn;
+      if (rr == 0.0) {
+        c = 1.0;
+        sn = c_make(0.0, 0.0);
+      } else if (ax == 0.0) {
+        c = 0.0;
+        sn = c_scale(c_conj(y), 1.0 / ay);
       } else {
-        y = A_(nn - 1, nn - 1);
-        w = A_(nn, nn - 1) * A_(nn - 1, nn);
-        if (l == nn - 1) {
-          p = 0.5 * (y - x);
-          q = p * p + w;
-          z = sqrt(fabs(q));
-          x += t;
-          if (q >= 0.0) {
-            z = p + sgn_of(z, p);
-            wr[nn - 1] = wr[nn] = x + z;
-            if (z != 0.0) wr[nn] = x - w / z;
-            wi[nn - 1] = wi[nn] = 0.0;
-          } else {
-            wr[nn - 1] = wr[nn] = x + p;
-            wi[nn - 1] = z;
-            wi[nn] = -z;
-          }
-          nn -= 2;
-        } else {
-          if (its == 30) return false;
-          if (its == 10 || its == 20) {
-            t += x;
-            for (int i = 0; i <= nn; ++i) A_(i, i) -= x;
-            s = fabs(A_(nn, nn - 1)) + fabs(A_(nn - 1, nn - 2));
-            y = x = 0.75 * s;
-            w = -0.4375 * s * s;
-          }
-          ++its;
-          int m;
-          for (m = nn - 2; m >= l; --m) {
-            z = A_(m, m);
-            r = x - z;
-            s = y - z;
-            p = (r * s - w) / A_(m + 1, m) + A_(m, m + 1);
-            q = A_(m + 1, m + 1) - z - r - s;
-            r = A_(m + 2, m + 1);
-            s = fabs(p) + fabs(q) + fabs(r);
-            p /= s;
-            q /= s;
-            r /= s;
-            if (m == l) break;
-            const double u = fabs(A_(m, m - 1)) * (fabs(q) + fabs(r));
-            const double v = fabs(p) * (fabs(A_(m - 1, m - 1)) + fabs(z) + fabs(A_(m + 1, m + 1)));
-            if (u + v == v) break;
-          }
-          for (int i = m + 2; i <= nn; ++i) {
-            A_(i, i - 2) = 0.0;
-            if (i != m + 2) A_(i, i - 3) = 0.0;
-          }
-          for (int k = m; k <= nn - 1; ++k) {
-            if (k != m) {
-              p = A_(k, k - 1);
-              q = A_(k + 1, k - 1);
-              r = 0.0;
-              if (k != nn - 1) r = A_(k + 2, k - 1);
-              if ((x = fabs(p) + fabs(q) + fabs(r)) != 0.0) {
-                p /= x;
-                q /= x;
-                r /= x;
-              }
-            }
-            if ((s = sgn_of(sqrt(p * p + q * q + r * r), p)) != 0.0) {
-              if (k == m) {
-                if (l != m) A_(k, k - 1) = -A_(k, k - 1);
-              } else {
-                A_(k, k - 1) = -s * x;
-              }
-              p += s;
-              x = p / s;
-              y = q / s;
-              z = r / s;
-              q /= p;
-              r /= p;
-              for (int j = k; j <= nn; ++j) {
-                p = A_(k, j) + q * A_(k + 1, j);
-                if (k != nn - 1) {
-                  p += r * A_(k + 2, j);
-                  A_(k + 2, j) -= p * z;
-                }
-                A_(k + 1, j) -= p * y;
-                A_(k, j) -= p * x;
-              }
-              const int mmin = nn < k + 3 ? nn : k + 3;
-              for (int i = l; i <= mmin; ++i) {
-                p = x * A_(i, k) + y * A_(i, k + 1);
-                if (k != nn - 1) {
-                  p += z * A_(i, k + 2);
-                  A_(i, k + 2) -= p * r;
-                }
-                A_(i, k + 1) -= p * q;
-                A_(i, k) -= p;
-              }
-            }
-          }
-        }
+        c = ax / rr;
+        sn = c_scale(c_mul(c_scale(x, 1.0 / ax), c_conj(y)), 1.0 / rr);
       }
-    } while (l < nn - 1);
+      for (int j = k; j <= hi; ++j) {
+        const cplx a1 = Z_(k, j), a2 = Z_(k + 1, j);
+        Z_(k, j) = c_add(c_scale(a1, c), c_mul(sn, a2));
+        Z_(k + 1, j) = c_sub(c_scale(a2, c), c_mul(c_conj(sn), a1));
+      }
+      gc[k] = c;
+      Z_(k + 1, k) = sn;
+    }
+    // RQ: apply G_k^H from the right, k = lo..hi-1
+    for (int k = lo; k < hi; ++k) {
+      const double c = gc[k];
+      const cplx sn = Z_(k + 1, k);
+      Z_(k + 1, k) = c_make(0.0, 0.0);
+      for (int i = lo; i <= k + 1; ++i) {
+        const cplx a1 = Z_(i, k), a2 = Z_(i, k + 1);
+        Z_(i, k) = c_add(c_scale(a1, c), c_mul(a2, c_conj(sn)));
+        Z_(i, k + 1) = c_sub(c_scale(a2, c), c_mul(a1, sn));
+      }
+    }
+    for (int i = lo; i <= hi; ++i) Z_(i, i) = c_add(Z_(i, i), mu);
   }
   return true;
-#undef A_
+#undef Z_
 }
 
 // Unit-norm eigenvector of the eigenvalue of largest modulus (first one on
@@ -269,8 +254,12 @@ PGM_HD int dominant_eigvec(const double* T, int n, int ld, double* v, double* wo
   double* xs = b + 2 * n;       // 2n
   for (int j = 0; j < n; ++j)
     for (int i = 0; i < n; ++i) h[i + j * n] = T[i + j * ld];
-  hessenberg(h, n, n);
-  if (!hqr(h, n, n, wr, wi)) return 1;
+  hessenberg_reduce(h, n, n);
+  if (!hessenberg_eigvals(h, n, n, wr, wi, m)) return 1;
+  // complex arithmetic leaves real eigenvalues with rounding-level imaginary
+  // parts once a complex shift was used
+  for (int i = 0; i < n; ++i)
+    if (fabs(wi[i]) <= 1e-13 * hypot(wr[i], wi[i])) wi[i] = 0.0;
   int dom = 0;
   double best = -1.0;
   for (int i = 0; i < n; ++i) {

@@ -315,7 +315,10 @@ __device__ int dcgs2_column(const Params& P, int k, const double* sa, double alp
     g->active = 0;
     return 0;
   }
-  P.s[k] = 1.0 / beta;
+  // beta == 0 without the breakdown exit (breakdown_scale = 0 or beta_cycle
+  // = 0, fixed iterations): continue with finite coefficients, as the
+  // reference's arnoldi_step does for hnext == 0 (gmres.cpp:60-63)
+  P.s[k] = beta > 0.0 ? 1.0 / beta : 0.0;
   return 1;
 }
 
@@ -345,7 +348,7 @@ __device__ void fin_dcgs2(const Params& P, int k, const double* red) {
   __syncthreads();
   if (!s_go) return;
   const double beta = s_beta;
-  const double ib = 1.0 / beta;
+  const double ib = beta > 0.0 ? 1.0 / beta : 0.0;
   if (k == 0) {
     // q_0 is final: column 0's first pass h1_0 = v_0 . y; u_1 = y - h1_0 v_0
     if (threadIdx.x == 0) {

@@ -1678,29 +1678,44 @@ __global__ void k_sell_compress(Sell A, int nslices, unsigned short* col16, unsi
 
 // Rows that read halo columns (global column < rb or >= re; columns ascending
 // per row): out[0] = last such row below, out[1] = first such row above.
-__global__ void k_halo_rows(const unsigned* rp, const unsigned* col, int n, unsigned rb,
-                            unsigned re, int* out) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const unsigned a = rp[i], b = rp[i + 1];
-    if (a == b) continue;
-    if (col[a] < rb) atomicMax(&out[0], i);
-    if (col[b - 1] >= re) atomicMin(&out[1], i);
-  }
-}
-
-__global__ void k_csr_to_sell(Sell A, double* val, unsigned* col, const unsigned* rp,
-                              const unsigned* ci, const double* v, unsigned col_shift,
-                              int nslices, int write_cols) {
+// Halo tiles (world > 1): the last row whose first column lies below the own
+// block and the first row whose last column lies above it, from the SELL
+// layout (32-bit local column ids, rows sorted ascending: entry t = 0 is the
+// row's first column, t = len - 1 its last).  Own local columns: [lo, hi).
+__global__ void k_halo_rows_sell(Sell A, int nslices, unsigned lo, unsigned hi, int* out) {
   const int lane = threadIdx.x & 31;
   const size_t s = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
   if (s >= (size_t)nslices) return;
+  const int len = (int)A.lane_len[s * 32 + lane];
+  const unsigned short ro = A.lane_row[s * 32 + lane];
+  if (ro == 0xFFFF || len == 0) return;
+  const unsigned long long base = A.sptr[s];
+  const int row = (int)((s / SPT) * TILE + ro);
+  const int tl = len - 1;
+  const unsigned c0 = A.col[base + lane * 4];
+  const unsigned c1 = A.col[base + (size_t)(tl >> 2) * 128 + lane * 4 + (tl & 3)];
+  if (c0 < lo) atomicMax(&out[0], row);
+  if (c1 >= hi) atomicMin(&out[1], row);
+}
+
+// CSR -> SELL gather for slices [s0, s0 + count): entry t of the lane that
+// holds row `row` is CSR entry rp[row] + t, read from ci / v at offset
+// (rp[row] + t - csr_base) — the caller's arrays (csr_base = 0) or a staged
+// chunk of them.  Padding entries get value 0 and column 0.
+__global__ void k_csr_to_sell(Sell A, double* val, unsigned* col, const unsigned* rp,
+                              const unsigned* ci, const double* v, unsigned col_shift,
+                              int s0, int count, unsigned long long csr_base, int write_cols) {
+  const int lane = threadIdx.x & 31;
+  const size_t sl = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  if (sl >= (size_t)count) return;
+  const size_t s = s0 + sl;
   const unsigned long long base = A.sptr[s];
   const int L = (int)((A.sptr[s + 1] - base) >> 5);
   const int len = (int)A.lane_len[s * 32 + lane];
   const unsigned short ro = A.lane_row[s * 32 + lane];
   const size_t tile = s / SPT;
   const size_t row = tile * TILE + ro;
-  const size_t start = (ro != 0xFFFF) ? rp[row] : 0;
+  const size_t start = (ro != 0xFFFF) ? (size_t)rp[row] - csr_base : 0;
   for (int t = 0; t < L; ++t) {
     const size_t idx = base + (size_t)(t >> 2) * 128 + lane * 4 + (t & 3);
     if (t < len) {

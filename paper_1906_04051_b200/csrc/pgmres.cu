@@ -59,6 +59,18 @@ Status dalloc(T** p, size_t count) {
   *p = nullptr;
   if (count == 0) count = 1;
   cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e == cudaErrorMemoryAllocation) {
+    // the stream-ordered pool keeps freed matrix memory (release threshold
+    // = inf): hand it back to the device and retry once
+    cudaGetLastError();
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      cudaDeviceSynchronize();
+      cudaMemPoolTrimTo(pool, 0);
+    }
+    e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     return Status{PGM_ENOMEM, std::string("cudaMalloc(") + std::to_string(count * sizeof(T)) +
@@ -202,7 +214,14 @@ struct pgm_matrix {
   unsigned short* col16 = nullptr;  // 16-bit column deltas (col freed when set)
   unsigned* lane_base = nullptr;
   unsigned* rp = nullptr;      // device CSR row_ptr (kept for value updates)
-  double* vstage = nullptr;    // device CSR values staging
+  // host-array transfers are staged through a bounded device buffer, a tile
+  // range at a time (no resident nnz-sized staging copy)
+  struct Chunk {
+    int s0, count;                // slices
+    unsigned long long lo, hi;    // CSR entries [lo, hi)
+  };
+  std::vector<Chunk> chunks;      // plan for host sources (built on first use)
+  unsigned long long chunk_cap = 0;
   unsigned col_shift = 0;
   // tiles [0, t_lo_end) and [t_hi_begin, ntiles) read halo rows; the rest is
   // interior (world > 1: runs while the halo planes are in flight)
@@ -905,10 +924,13 @@ Status solve_impl(pgm_context* ctx, pgm_matrix* A, pgm_deflator* dflt, const dou
   if (!A || A->ctx != ctx) return einval("pgm_solve: matrix belongs to another context");
   if (A->n != ctx->n) return einval("pgm_solve: matrix rows do not match the partition");
   const bool harvest = dflt != nullptr;
-  if (harvest && cfg->m > (uint32_t)MAX_M)
-    return einval("pgm_solve: deflated restart length m > " + std::to_string(MAX_M) +
-                  " is not supported on the device harvest path");
-  if (!harvest && cfg->m > 4096) return einval("pgm_solve: m too large");
+  // the finishers and update passes keep a cycle's Hessenberg column and
+  // coefficients in shared memory (MAX_M + O(1) doubles), the Ritz harvest
+  // keeps [H | H^-1]: every path is bounded by MAX_M (BASELINE's largest
+  // restart length is 100)
+  if (cfg->m > (uint32_t)MAX_M)
+    return einval("pgm_solve: restart length m > " + std::to_string(MAX_M) +
+                  " is not supported on the device path");
   pgm_deflator* d = harvest ? dflt : ctx->dummy;
   if (d->ctx != ctx) return einval("pgm_solve: deflator belongs to another context");
   const int m = (int)cfg->m;
@@ -996,6 +1018,85 @@ Status solve_impl(pgm_context* ctx, pgm_matrix* A, pgm_deflator* dflt, const dou
 // ---------------------------------------------------------------------------
 // Matrix upload: CSR (owned rows, global columns) -> SELL-32 tiles, layout
 // built on the device (k_sell_layout: per-tile stable sort by row length).
+// CSR values (and, on upload, column ids) -> the SELL arrays.  Device
+// sources are gathered in place by one launch; host sources go through a
+// bounded staging buffer one tile range at a time (<= STAGE_ENTRIES CSR
+// entries, or one tile if a single tile holds more), so no nnz-sized staging
+// copy is ever resident.  rp_src: the caller's row_ptr (host or device, as
+// `dev` says); a host plan needs the host row_ptr, so a device-uploaded
+// matrix that later receives host values copies row_ptr back once.
+constexpr unsigned long long STAGE_ENTRIES = 1ull << 25;  // 32 M entries: 384 MB
+
+Status gather_values(pgm_context* ctx, pgm_matrix* M, const uint32_t* rp_src,
+                     const uint32_t* ci_src, const double* v_src, bool dev, bool write_cols) {
+  cudaStream_t st = ctx->stream;
+  if (M->nslices == 0) return {};
+  const int threads = 256;
+  if (dev) {
+    const size_t blocks = ((size_t)M->nslices * 32 + threads - 1) / threads;
+    k_csr_to_sell<<<(unsigned)blocks, threads, 0, st>>>(M->view(), M->val, M->col, M->rp,
+                                                        ci_src, v_src, M->col_shift, 0,
+                                                        M->nslices, 0ull, write_cols ? 1 : 0);
+    CU(cudaGetLastError());
+    return {};
+  }
+  if (M->chunks.empty()) {
+    std::vector<uint32_t> hrp;
+    const uint32_t* rp = rp_src;
+    if (!rp) {
+      hrp.resize((size_t)M->n + 1);
+      CU(cudaMemcpyAsync(hrp.data(), M->rp, 4 * ((size_t)M->n + 1), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      rp = hrp.data();
+    }
+    unsigned long long cap = 0;
+    int t = 0;
+    while (t < M->ntiles) {
+      const int t0 = t;
+      const unsigned long long lo = rp[(size_t)t0 * TILE];
+      unsigned long long hi = lo;
+      while (t < M->ntiles) {
+        const size_t row_end = std::min<size_t>(M->n, (size_t)(t + 1) * TILE);
+        const unsigned long long h = rp[row_end];
+        if (t > t0 && h - lo > STAGE_ENTRIES) break;
+        hi = h;
+        ++t;
+      }
+      M->chunks.push_back({t0 * SPT, (t - t0) * SPT, lo, hi});
+      cap = std::max(cap, hi - lo);
+    }
+    M->chunk_cap = cap;
+  }
+  double* sv = nullptr;
+  unsigned* sc = nullptr;
+  const size_t cap = std::max<unsigned long long>(M->chunk_cap, 1);
+  TRY(dalloc_async(&sv, cap, st));
+  Status s;
+  if (write_cols) s = dalloc_async(&sc, cap, st);
+  cudaError_t e = cudaSuccess;
+  for (const auto& c : M->chunks) {
+    if (s.code || e != cudaSuccess) break;
+    const size_t cnt = c.hi - c.lo;
+    // stream order makes reuse of the one staging buffer safe: the next
+    // copy starts after the previous chunk's gather
+    e = cudaMemcpyAsync(sv, v_src + c.lo, 8 * cnt, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && write_cols)
+      e = cudaMemcpyAsync(sc, ci_src + c.lo, 4 * cnt, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+      const size_t blocks = ((size_t)c.count * 32 + threads - 1) / threads;
+      k_csr_to_sell<<<(unsigned)blocks, threads, 0, st>>>(M->view(), M->val, M->col, M->rp, sc,
+                                                          sv, M->col_shift, c.s0, c.count, c.lo,
+                                                          write_cols ? 1 : 0);
+      e = cudaGetLastError();
+    }
+  }
+  dfree_async(sv, st);
+  dfree_async(sc, st);
+  if (s.code) return s;
+  CU(e);
+  return {};
+}
+
 Status matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags, pgm_matrix** out) {
   if (!a || !out) return einval("pgm_matrix_upload: null argument");
   if (a->n != ctx->n)
@@ -1055,20 +1156,11 @@ Status matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags, pgm
   M->stored = stored;
   if ((s = dalloc_async(&M->val, M->stored, st)).code) return cleanup(s);
   if ((s = dalloc_async(&M->col, M->stored, st)).code) return cleanup(s);
-  if ((s = dalloc_async(&M->vstage, a->nnz, st)).code) return cleanup(s);
-  unsigned* cstage = nullptr;
-  if ((s = dalloc_async(&cstage, a->nnz, st)).code) return cleanup(s);
-  e = e ? e : cudaMemcpyAsync(M->vstage, a->values, 8 * a->nnz, kind, st);
-  e = e ? e : cudaMemcpyAsync(cstage, a->col_idx, 4 * a->nnz, kind, st);
-  if (e != cudaSuccess) {
-    cudaFreeAsync(cstage, st);
-    return cleanup(Status{PGM_ECUDA, std::string("upload: ") + cudaGetErrorString(e)});
-  }
+  if ((s = gather_values(ctx, M, a->row_ptr, a->col_idx, a->values, dev, true)).code)
+    return cleanup(s);
   const int threads = 256;
   const size_t blocks = ((size_t)M->nslices * 32 + threads - 1) / threads;
-  if (M->nslices > 0)
-    k_csr_to_sell<<<(unsigned)blocks, threads, 0, st>>>(M->view(), M->val, M->col, M->rp, cstage,
-                                                        M->vstage, M->col_shift, M->nslices, 1);
+  unsigned* col32 = M->col;
   e = cudaGetLastError();
   if (e == cudaSuccess && M->nslices > 0 && !std::getenv("PGMRES_NO_C16")) {
     // 16-bit column deltas when every gap fits (10 instead of 12 B / nonzero)
@@ -1089,7 +1181,7 @@ Status matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags, pgm
         k_sell_compress<<<(unsigned)blocks, threads, 0, st>>>(v32, M->nslices, M->col16,
                                                               M->lane_base);
         e = cudaGetLastError();
-        if (e == cudaSuccess) dfree_async(M->col, st);
+        if (e == cudaSuccess) M->col = nullptr;  // col32 freed after the halo scan
       } else {
         cudaGetLastError();  // not enough memory: keep 32-bit columns
         dfree_async(M->col16, st);
@@ -1100,20 +1192,25 @@ Status matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags, pgm
   M->t_lo_end = 0;
   M->t_hi_begin = M->ntiles;
   if (e == cudaSuccess && ctx->world > 1 && a->n > 0) {
+    // halo tiles from the 32-bit SELL columns (k_sell_compress keeps `col`
+    // until the stream reaches its free)
     int h[2] = {-1, (int)a->n};
     int* dh = nullptr;
     e = cudaMalloc(&dh, sizeof(h));
     if (e == cudaSuccess) e = cudaMemcpyAsync(dh, h, sizeof(h), cudaMemcpyHostToDevice, st);
+    Sell v32 = M->view();
+    v32.col16 = nullptr;
+    v32.col = col32;
     if (e == cudaSuccess)
-      k_halo_rows<<<ctx->nsm * 4, 256, 0, st>>>(M->rp, cstage, (int)a->n, ctx->part.row_begin,
-                                                ctx->part.row_end, dh);
+      k_halo_rows_sell<<<(unsigned)blocks, threads, 0, st>>>(
+          v32, M->nslices, ctx->part.halo_lo, ctx->part.halo_lo + (unsigned)a->n, dh);
     if (e == cudaSuccess) e = cudaMemcpyAsync(h, dh, sizeof(h), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFree(dh);
     M->t_lo_end = (h[0] + 1 + TILE - 1) / TILE;
     M->t_hi_begin = std::max(M->t_lo_end, h[1] / TILE);
   }
-  cudaFreeAsync(cstage, st);
+  if (col32 != M->col) dfree_async(col32, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess)
     return cleanup(Status{PGM_ECUDA, std::string("csr->sell: ") + cudaGetErrorString(e)});
@@ -1449,16 +1546,10 @@ pgm_status pgm_matrix_update_values(pgm_matrix* a, const double* values, int32_t
   }
   pgm_context* ctx = a->ctx;
   cudaStream_t st = ctx->stream;
-  cudaError_t e = cudaMemcpyAsync(a->vstage, values, 8 * a->nnz,
-                                  (flags & PGM_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice
-                                                            : cudaMemcpyHostToDevice,
-                                  st);
-  if (e == cudaSuccess && a->nslices > 0) {
-    const size_t blocks = ((size_t)a->nslices * 32 + 255) / 256;
-    k_csr_to_sell<<<(unsigned)blocks, 256, 0, st>>>(a->view(), a->val, a->col, a->rp, nullptr,
-                                                    a->vstage, a->col_shift, a->nslices, 0);
-    e = cudaGetLastError();
-  }
+  Status s = gather_values(ctx, a, nullptr, nullptr, values, (flags & PGM_DEVICE_PTRS) != 0,
+                           false);
+  if (s.code) return fail(ctx, s);
+  cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return fail(ctx, Status{PGM_ECUDA, cudaGetErrorString(e)});
   return PGM_OK;
@@ -1479,7 +1570,6 @@ void pgm_matrix_destroy(pgm_matrix* a) {
     dfree_async(a->col16, st);
     dfree_async(a->lane_base, st);
     dfree_async(a->rp, st);
-    dfree_async(a->vstage, st);
   } else {  // its context was destroyed first: plain (synchronous) frees
     cudaDeviceSynchronize();
     dfree(a->sptr);
@@ -1490,7 +1580,6 @@ void pgm_matrix_destroy(pgm_matrix* a) {
     dfree(a->col16);
     dfree(a->lane_base);
     dfree(a->rp);
-    dfree(a->vstage);
   }
   delete a;
 }
@@ -1501,8 +1590,8 @@ pgm_status pgm_matrix_info(const pgm_matrix* a, uint32_t* n, uint64_t* nnz, uint
   if (nnz) *nnz = a->nnz;
   if (stored) *stored = a->stored;
   if (device_bytes)
-    *device_bytes = a->stored * 12 + (uint64_t)a->nslices * (8 + 32 * 6) + 4ull * (a->n + 1) +
-                    8ull * a->nnz;
+    *device_bytes = a->stored * (a->col16 ? 10 : 12) +
+                    (uint64_t)a->nslices * (8 + 32 * (a->col16 ? 10 : 6)) + 4ull * (a->n + 1);
   return PGM_OK;
 }
 

@@ -9,9 +9,9 @@ int h_dominant_eigvec(const double* T, int n, double* v) {
   return pgm::dense::dominant_eigvec(T, n, n, v, work.data(), iw.data());
 }
 int h_eigvals(const double* T, int n, double* wr, double* wi) {
-  std::vector<double> h(T, T + n * n);
-  pgm::dense::hessenberg(h.data(), n, n);
-  return pgm::dense::hqr(h.data(), n, n, wr, wi) ? 0 : 1;
+  std::vector<double> h(T, T + n * n), z(2 * n * n + n);
+  pgm::dense::hessenberg_reduce(h.data(), n, n);
+  return pgm::dense::hessenberg_eigvals(h.data(), n, n, wr, wi, z.data()) ? 0 : 1;
 }
 void h_invert(const double* A, int n, double* inv) {
   std::vector<double> a(A, A + n * n), w(n);
