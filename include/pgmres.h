@@ -168,6 +168,23 @@ pgm_status pgm_solve(pgm_context* ctx, pgm_matrix* a, pgm_deflator* d, const dou
                      double* x, const pgm_gmres_config* cfg, int32_t flags, pgm_report* rep);
 void pgm_report_free(pgm_report* rep);
 
+/* Restart observer — the RestartHook of gmres_restarted (gmres.hpp:94-113,
+ * gmres.cpp:189) for audits such as acceptance.cpp:100-122 (criterion 8):
+ * called on the host after every restart cycle's x update and deflation
+ * harvest, before the explicit residual, with the 0-based cycle index and
+ * the Arnoldi steps it completed.  Inside the callback the cycle's basis and
+ * Hessenberg matrix can be read (below) and the deflator inspected
+ * (pgm_deflator_info / _history / _basis); no other pgm_* call on this
+ * context is allowed.  A nonzero return stops the solve with PGM_ESTATE.
+ * cb = NULL removes the observer (then nothing synchronises mid-solve). */
+typedef int32_t (*pgm_restart_observer)(void* user, uint32_t restart, uint32_t steps);
+pgm_status pgm_set_restart_observer(pgm_context* ctx, pgm_restart_observer cb, void* user);
+/* v_j (j < steps, owned rows) into host memory: GmresWorkspace::basis(j). */
+pgm_status pgm_restart_basis(pgm_context* ctx, uint32_t j, double* out);
+/* The cycle's unrotated Hessenberg matrix, (m+1) x m column-major
+ * (GmresWorkspace::hess(i, j) = out[i + j (m+1)], valid for j < steps). */
+pgm_status pgm_restart_hessenberg(pgm_context* ctx, double* out);
+
 /* 128-byte ncclUniqueId for pgm_context_config.nccl_id (call on rank 0 and
  * broadcast it, e.g. with torch.distributed). */
 pgm_status pgm_nccl_unique_id(void* out128);

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../pgmres.h"
+#include "pattern_hash.hpp"
 
 namespace pgmres {
 
@@ -113,7 +114,7 @@ class DeviceExecutor {
   DeviceExecutor(int device, std::uint32_t n_axis, int rank, int world, const void* nccl_id)
       : device_(device), n_axis_(n_axis), rank_(rank), world_(world), nccl_id_(nccl_id) {}
   ~DeviceExecutor() {
-    for (auto& c : cache_) pgm_matrix_destroy(c.mat);
+    release();
     if (ctx_) pgm_context_destroy(ctx_);
   }
   DeviceExecutor(const DeviceExecutor&) = delete;
@@ -131,21 +132,32 @@ class DeviceExecutor {
   }
   pgm_context* handle() const { return ctx_; }
 
-  // Upload (or refresh the values of) a host CSR matrix: the sparsity pattern is
-  // uploaded once per matrix object, later calls only move the values
-  // (Newton re-assembles values on a fixed pattern, assembly.cpp:253).
+  // Upload (or refresh the values of) a host CSR matrix.  ONE device matrix
+  // stays resident, keyed on the pattern's identity (n, nnz, hash of row_ptr
+  // and col_idx — content, not the host object's address): the same pattern
+  // only moves the values (Newton re-assembles values on a fixed pattern,
+  // assembly.cpp:253); a new pattern releases the previous device copy.
   pgm_matrix* matrix(const CsrMatrix& A) {
     pgm_context* ctx = context(world_ == 1 ? A.n : n_global_);
-    for (auto& c : cache_)
-      if (c.key == &A && c.nnz == A.nnz() && c.n == A.n) {
-        detail::check(pgm_matrix_update_values(c.mat, A.values.data(), 0), ctx);
-        return c.mat;
-      }
+    if (A.row_ptr.size() != std::size_t(A.n) + 1)
+      throw std::invalid_argument("CsrMatrix: row_ptr must have n + 1 entries");
+    const std::uint64_t h =
+        detail::pattern_hash(A.row_ptr.data(), A.n, A.col_idx.data(), A.col_idx.size());
+    if (cur_.mat && cur_.n == A.n && cur_.nnz == A.nnz() && cur_.hash == h) {
+      detail::check(pgm_matrix_update_values(cur_.mat, A.values.data(), 0), ctx);
+      return cur_.mat;
+    }
+    release();
     pgm_csr_view v{A.n, A.nnz(), A.row_ptr.data(), A.col_idx.data(), A.values.data()};
     pgm_matrix* m = nullptr;
     detail::check(pgm_matrix_upload(ctx, &v, 0, &m), ctx);
-    cache_.push_back({&A, A.n, A.nnz(), m});
+    cur_ = Entry{A.n, A.nnz(), h, m};
     return m;
+  }
+  // Drop the resident device matrix (the next solve uploads again).
+  void release() {
+    if (cur_.mat) pgm_matrix_destroy(cur_.mat);
+    cur_ = Entry{};
   }
 
   void spmv(const CsrMatrix& A, const DenseVector& x, DenseVector& y) {
@@ -156,10 +168,9 @@ class DeviceExecutor {
 
  private:
   struct Entry {
-    const CsrMatrix* key;
-    index_t n;
-    std::uint64_t nnz;
-    pgm_matrix* mat;
+    index_t n = 0;
+    std::uint64_t nnz = 0, hash = 0;
+    pgm_matrix* mat = nullptr;
   };
   int device_ = 0;
   std::uint32_t n_axis_ = 0;
@@ -167,7 +178,7 @@ class DeviceExecutor {
   const void* nccl_id_ = nullptr;
   index_t n_global_ = 0;
   pgm_context* ctx_ = nullptr;
-  std::vector<Entry> cache_;
+  Entry cur_;
 };
 
 class Deflator {

@@ -83,8 +83,12 @@ EXPORTS = [
     "pgm_context_launch_count", "pgm_context_set_profiling", "pgm_context_profile",
     "pgm_bratu_nnz", "pgm_bratu_assemble", "pgm_nccl_unique_id", "pgm_loopback_create",
     "pgm_loopback_destroy", "pgm_newton_solve", "pgm_newton_report_free", "pgm_peer_export",
-    "pgm_peer_import",
+    "pgm_peer_import", "pgm_set_restart_observer", "pgm_restart_basis",
+    "pgm_restart_hessenberg",
 ]
+
+# pgm_restart_observer: int32 (*)(void* user, uint32 restart, uint32 steps)
+RestartObserver = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_uint32, C.c_uint32)
 
 _lib = None
 
@@ -140,6 +144,9 @@ def lib():
         "pgm_newton_report_free": ([C.POINTER(NewtonReportC)], None),
         "pgm_peer_export": ([vp, vp], C.c_int),
         "pgm_peer_import": ([vp, vp], C.c_int),
+        "pgm_set_restart_observer": ([vp, RestartObserver, vp], C.c_int),
+        "pgm_restart_basis": ([vp, u32, vp], C.c_int),
+        "pgm_restart_hessenberg": ([vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

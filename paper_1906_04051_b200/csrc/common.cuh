@@ -44,6 +44,7 @@ struct GState {
   int steps;        // Arnoldi steps completed in the current cycle
   int lucky;        // cycle ended on h < breakdown_scale * beta
   int converged, breakdown, restarts, n_inner;
+  int dc_fallback;  // DCGS2 remainder hit rounding level: later cycles use CGS2
   unsigned long long total_inner;
   double beta0, beta, beta_cycle, final_relative;
   // configuration (GmresConfig)

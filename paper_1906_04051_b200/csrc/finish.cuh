@@ -261,7 +261,21 @@ __device__ int dcgs2_column(const Params& P, int k, const double* sa, double alp
   const size_t col = (size_t)(k - 1) * (m + 1);
   double na2 = 0.0;
   for (int l = 0; l < k; ++l) na2 += sa[l] * sa[l];
-  const double beta = sqrt(fmax(alpha - na2, 0.0));
+  // Pythagorean remainder ||u_k - Q a||^2 = alpha - ||a||^2.  When it sits at
+  // rounding level of alpha the value carries no digits (it can even clamp to
+  // 0).  If the bound sqrt(floor) is itself below the breakdown threshold the
+  // Krylov space is exhausted (gmres.cpp:173 fires for any true value);
+  // otherwise the step is ambiguous: the cycle closes here (not a lucky
+  // breakdown) and later cycles run the CGS2 step, whose remainder norm is
+  // formed explicitly (pass B) — no false breakdown at the rounding floor.
+  const double diff = alpha - na2;
+  const double floor2 = 4.0 * (k + 1) * 2.220446049250313e-16 * alpha;
+  bool ambiguous = false;
+  double beta = sqrt(fmax(diff, 0.0));
+  if (diff <= floor2 && alpha > 0.0 && sqrt(floor2) >= g->breakdown_scale * g->beta_cycle) {
+    ambiguous = true;
+    beta = sqrt(floor2);
+  }
   *s_beta = beta;
   for (int l = 0; l < k; ++l) {
     const double h = P.h_orig[col + l] + sa[l];
@@ -305,7 +319,10 @@ __device__ int dcgs2_column(const Params& P, int k, const double* sa, double alp
   P.rec_mon[idx] = monitored;
   g->steps = kk + 1;
   bool stop = close || kk + 1 >= m;
-  if (beta < g->breakdown_scale * g->beta_cycle) {
+  if (ambiguous) {
+    g->dc_fallback = 1;
+    stop = true;
+  } else if (beta < g->breakdown_scale * g->beta_cycle) {
     g->lucky = 1;
     stop = true;
   } else if (!g->fixed && monitored <= g->rel_tol * g->beta0) {

@@ -1285,6 +1285,9 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
   const int k = g->steps;
   const int tid = threadIdx.x;
   __shared__ double s_red[32];
+  // a new harvest: the previous truncation's rotation has been applied; a
+  // rejected push this time must not re-apply it (k_rotate runs regardless)
+  if (tid == 0) d->rotate = 0;
   if (k == 0) {
     if (tid == 0) {
       d->skipped++;

@@ -141,6 +141,12 @@ struct pgm_loopback {
 
 struct pgm_context {
   int device = 0, rank = 0, world = 1;
+  // restart observer (pgm_set_restart_observer): called on the host after
+  // each cycle's x update and deflation harvest, before the explicit residual
+  pgm_restart_observer obs = nullptr;
+  void* obs_user = nullptr;
+  bool in_obs = false;
+  int obs_steps = 0;
   // collective mode: reductions go through red_out + allreduce + k_finish.
   // world > 1, or a 1-rank NCCL communicator (world = 1 with an nccl_id:
   // exercises the NCCL path on one GPU).
@@ -774,8 +780,15 @@ Status finish_global(pgm_context* ctx, const Params& P, int k, int nv) {
 
 // One restart cycle of the solve: m Arnoldi steps (3 fused kernels each), the
 // x update, the deflation harvest and the explicit residual.
+Status enqueue_residual(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Params& P) {
+  if (ctx->world > 1) TRY(halo_exchange(ctx, HV_X));
+  TRY(launch_spmv(ctx, A, P, ResidualEpi{0}, d->R1 + 1));
+  TRY(finish_global<101>(ctx, P, 0, d->R1 + 1));
+  return {};
+}
+
 Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Params& P,
-                     bool harvest) {
+                     bool harvest, bool residual = true) {
   const int m = ctx->ws_m;
   const int R1 = d->R1;
   const bool overlap = ctx->world > 1 && A->t_hi_begin > A->t_lo_end;
@@ -869,9 +882,24 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
     ctx->launches++;
     CU(cudaGetLastError());
   }
-  if (ctx->world > 1) TRY(halo_exchange(ctx, HV_X));
-  TRY(launch_spmv(ctx, A, P, ResidualEpi{0}, R1 + 1));
-  TRY(finish_global<101>(ctx, P, 0, R1 + 1));
+  if (residual) TRY(enqueue_residual(ctx, A, d, P));
+  return {};
+}
+
+// Restart observer: the cycle (x update + harvest) has been enqueued; wait for
+// it and hand the host the restart index and step count.  The basis and H stay
+// readable (pgm_restart_basis / pgm_restart_hessenberg) until the callback
+// returns; the explicit residual (which reuses W_0) is enqueued afterwards.
+Status observe_restart(pgm_context* ctx) {
+  CU(cudaStreamSynchronize(ctx->stream));
+  GState gs;
+  CU(cudaMemcpy(&gs, ctx->g, sizeof(GState), cudaMemcpyDeviceToHost));
+  if (gs.error) return {};
+  ctx->in_obs = true;
+  ctx->obs_steps = gs.steps;
+  const int rc = ctx->obs(ctx->obs_user, (uint32_t)gs.restart, (uint32_t)gs.steps);
+  ctx->in_obs = false;
+  if (rc != 0) return Status{PGM_ESTATE, "restart observer requested the solve to stop"};
   return {};
 }
 
@@ -979,8 +1007,19 @@ Status solve_impl(pgm_context* ctx, pgm_matrix* A, pgm_deflator* dflt, const dou
   TRY(read_status(ctx));
   while (!ctx->h_status->done) {
     ctx->prof_cycle = ctx->h_status->restart;
-    TRY(enqueue_cycle(ctx, A, d, P, harvest));
+    if (ctx->obs) {
+      TRY(enqueue_cycle(ctx, A, d, P, harvest, false));
+      TRY(observe_restart(ctx));
+      TRY(enqueue_residual(ctx, A, d, P));
+    } else {
+      TRY(enqueue_cycle(ctx, A, d, P, harvest));
+    }
     TRY(read_status(ctx));
+    // a DCGS2 remainder at rounding level (finish.cuh dcgs2_column) closed the
+    // cycle early: the remaining cycles of this solve run the CGS2 step
+    if (ctx->dc_now && ctx->h_status->dc_fallback) ctx->dc_now = false;
+    if (const char* e = std::getenv("PGMRES_DC_SWITCH_AT"))  // test knob: forced switch
+      if (ctx->h_status->restart >= std::atoi(e)) ctx->dc_now = false;
   }
   CU(cudaEventRecord(ctx->ev1, ctx->stream));
   const GState hs = *ctx->h_status;
@@ -1854,6 +1893,45 @@ pgm_status pgm_deflator_apply(pgm_deflator* d, const double* v, double* w, int32
   };
   Status s = run();
   return s.code ? fail(ctx, s) : PGM_OK;
+}
+
+pgm_status pgm_set_restart_observer(pgm_context* ctx, pgm_restart_observer cb, void* user) {
+  if (!ctx) return PGM_EINVAL;
+  ctx->obs = cb;
+  ctx->obs_user = user;
+  return PGM_OK;
+}
+
+pgm_status pgm_restart_basis(pgm_context* ctx, uint32_t j, double* out) {
+  if (!ctx || !out) return PGM_EINVAL;
+  if (!ctx->in_obs) {
+    ctx->err = "pgm_restart_basis: only valid inside a restart observer";
+    return PGM_ESTATE;
+  }
+  if ((int)j >= ctx->obs_steps) {
+    ctx->err = "pgm_restart_basis: basis vector " + std::to_string(j) + " of " +
+               std::to_string(ctx->obs_steps);
+    return PGM_EINVAL;
+  }
+  double sj = 0.0;
+  cudaError_t e = cudaMemcpy(&sj, ctx->s + j, sizeof(double), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(out, ctx->V + (size_t)j * ctx->ld + ctx->lo, 8 * ctx->n, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return fail(ctx, Status{PGM_ECUDA, cudaGetErrorString(e)});
+  for (size_t i = 0; i < ctx->n; ++i) out[i] *= sj;  // v_j = s_j W_j (lazy scale)
+  return PGM_OK;
+}
+
+pgm_status pgm_restart_hessenberg(pgm_context* ctx, double* out) {
+  if (!ctx || !out) return PGM_EINVAL;
+  if (!ctx->in_obs) {
+    ctx->err = "pgm_restart_hessenberg: only valid inside a restart observer";
+    return PGM_ESTATE;
+  }
+  const size_t hm = (size_t)(ctx->ws_m + 1) * ctx->ws_m;
+  cudaError_t e = cudaMemcpy(out, ctx->h_orig, 8 * hm, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return fail(ctx, Status{PGM_ECUDA, cudaGetErrorString(e)});
+  return PGM_OK;
 }
 
 pgm_status pgm_solve(pgm_context* ctx, pgm_matrix* a, pgm_deflator* d, const double* b, double* x,

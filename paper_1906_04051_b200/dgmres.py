@@ -528,7 +528,46 @@ class Deflator:
             pass
 
 
-def _solve(A, b, x, cfg: GmresConfig, d: Deflator | None, ex: DeviceExecutor) -> GmresReport:
+class RestartWorkspace:
+    """GmresWorkspace as a restart hook sees it (gmres.hpp:49-92 accessors):
+    the finished cycle's basis vectors and unrotated Hessenberg matrix, read
+    from the device on demand while the hook runs."""
+
+    def __init__(self, ex: DeviceExecutor, m: int, steps: int):
+        self._ex, self._m, self._steps = ex, m, steps
+        self._h = None
+
+    def n(self) -> int:
+        return self._ex.n_own
+
+    def m(self) -> int:
+        return self._m
+
+    def basis(self, j: int) -> np.ndarray:
+        out = np.empty(self._ex.n_own)
+        _check(capi.lib().pgm_restart_basis(self._ex.handle, int(j), out.ctypes.data),
+               self._ex.handle)
+        return out
+
+    def hess(self, i: int, j: int) -> float:
+        if self._h is None:
+            h = np.empty((self._m + 1) * self._m)
+            _check(capi.lib().pgm_restart_hessenberg(self._ex.handle, h.ctypes.data),
+                   self._ex.handle)
+            self._h = h
+        return float(self._h[i + j * (self._m + 1)])
+
+
+@dataclass
+class RestartContext:
+    """gmres.hpp:94-98."""
+    ws: RestartWorkspace
+    steps: int
+    restart: int
+
+
+def _solve(A, b, x, cfg: GmresConfig, d: Deflator | None, ex: DeviceExecutor,
+           hook=None) -> GmresReport:
     if cfg.m == 0:
         raise ValueError("GmresWorkspace: m must be positive")
     dA = A if isinstance(A, DeviceCsr) else DeviceCsr(ex, A)
@@ -547,8 +586,28 @@ def _solve(A, b, x, cfg: GmresConfig, d: Deflator | None, ex: DeviceExecutor) ->
     rep = capi.ReportC()
     c = cfg._c()
     L = capi.lib()
-    code = L.pgm_solve(ex.handle, dA.handle, d._h if d is not None else None, bp, xp,
-                       C.byref(c), f1, C.byref(rep))
+    cb = None
+    failure = []
+    if hook is not None:
+        def _observe(_user, restart, steps):
+            try:
+                hook(RestartContext(RestartWorkspace(ex, int(cfg.m), int(steps)), int(steps),
+                                    int(restart)))
+                return 0
+            except BaseException as e:  # re-raised after the solve stops
+                failure.append(e)
+                return 1
+        cb = capi.RestartObserver(_observe)
+        _check(L.pgm_set_restart_observer(ex.handle, cb, None), ex.handle)
+    try:
+        code = L.pgm_solve(ex.handle, dA.handle, d._h if d is not None else None, bp, xp,
+                           C.byref(c), f1, C.byref(rep))
+    finally:
+        if cb is not None:
+            L.pgm_set_restart_observer(ex.handle, capi.RestartObserver(), None)
+    if failure:
+        L.pgm_report_free(C.byref(rep))
+        raise failure[0]
     _check(code, ex.handle)
     del host_x
     try:
@@ -568,26 +627,30 @@ def _solve(A, b, x, cfg: GmresConfig, d: Deflator | None, ex: DeviceExecutor) ->
     return out
 
 
-def deflated_gmres(A, b, x, cfg: GmresConfig, d: Deflator, ex: DeviceExecutor) -> GmresReport:
-    """deflation.hpp:97-98.  x: initial guess in, iterate out (in place)."""
+def deflated_gmres(A, b, x, cfg: GmresConfig, d: Deflator, ex: DeviceExecutor,
+                   observer=None) -> GmresReport:
+    """deflation.hpp:97-98.  x: initial guess in, iterate out (in place).
+    observer: optional restart hook called with a RestartContext after every
+    cycle's x update and device harvest (the criterion-8 audit of
+    acceptance.cpp:100-122 runs here: d.rank(), d.basis(), ...)."""
     if d is None:
         raise ValueError("deflated_gmres needs a Deflator")
-    return _solve(A, b, x, cfg, d, ex)
+    return _solve(A, b, x, cfg, d, ex, observer)
 
 
 def gmres_restarted(opA, opM, b, x, cfg: GmresConfig, ex: DeviceExecutor,
                     hook=None) -> GmresReport:
     """gmres.hpp:110-113 for the production operator pair (opA = CSR SpMV,
-    opM = nullptr).  Arbitrary std::function operators and hooks stay on the
-    reference; the device path accepts only matrices (no CPU fallback)."""
+    opM = nullptr).  Arbitrary std::function operators stay on the reference;
+    the device path accepts only matrices (no CPU fallback).  hook: a restart
+    observer (gmres.hpp:94-103) called with a RestartContext after every
+    cycle's x update, reading the cycle's basis / Hessenberg from the device."""
     if opM is not None:
         raise ValueError("gmres_restarted: the device path takes opM=None; "
                          "use deflated_gmres for the deflation preconditioner")
-    if hook is not None:
-        raise ValueError("gmres_restarted: restart hooks are not supported on the device path")
     if not isinstance(opA, (CsrMatrix, DeviceCsr)):
         raise ValueError("gmres_restarted: opA must be a CsrMatrix or DeviceCsr")
-    return _solve(opA, b, x, cfg, None, ex)
+    return _solve(opA, b, x, cfg, None, ex, hook)
 
 
 # ---------------------------------------------------------------------------

@@ -639,3 +639,53 @@ def test_cgs2_path_still_matches(torch_cuda, ref, golden, monkeypatch, variant):
     pg.deflated_gmres(A2, b2, x2, pg.GmresConfig(m=4, max_restarts=24, fixed_iterations=True), d2,
                       pg.DeviceExecutor())
     assert [h.r for h in d2.history()] == list(gt["hist_r"])
+
+
+@pytest.mark.slow
+def test_ne200_fixed_cycles_and_fit(torch_cuda, golden):
+    """BASELINE config 5's largest mesh, n_e = 200 ("8000^2": 64,481,201 DOF,
+    4,073,625,625 nnz — gaps exceed 16 bits, so the 32-bit column layout).
+    (1) Deflated GMRES(20), 2 fixed cycles, against the reference run on the
+    GPU box's host (tests/golden/make_golden_ne200.py): histories within
+    1e-10 * beta0, x (every 64th entry) and per-plane norms within 1e-8.
+    (2) BASELINE's largest restart length m = 100 fits in HBM next to the
+    matrix (no resident CSR staging): 2 fixed deflated cycles, monitored and
+    explicit residuals consistent at every cycle end."""
+    import os
+
+    torch = torch_cuda
+    if not os.path.exists(os.path.join(os.path.dirname(__file__), "golden", "ne200_fixed.npz")):
+        pytest.skip("ne200 golden not generated")
+    g = golden("ne200_fixed")
+    ex = pg.DeviceExecutor()
+    A, b = ex.assemble_bratu(200, 6.8, device=True)
+    dA = ex.upload(A)
+    del A
+    torch.cuda.empty_cache()
+    info = dA.info()
+    assert info["nnz"] == 4073625625
+    assert info["device_bytes"] >= 12 * info["stored"]  # 32-bit column ids
+    x = torch.zeros(ex.n_own, dtype=torch.float64, device="cuda")
+    cfg = pg.GmresConfig(m=20, max_restarts=2, fixed_iterations=True)
+    d = pg.Deflator(pg.DeflationConfig(), ex)
+    rep = pg.deflated_gmres(dA, b, x, cfg, d, ex)
+    b0 = float(g["beta0"])
+    assert rep.beta0 == pytest.approx(b0, rel=1e-12)
+    assert rep.total_inner == int(g["total_inner"]) and rep.restarts == int(g["restarts"])
+    assert np.max(np.abs(rep.monitored - g["monitored"])) <= HIST_TOL * b0
+    assert np.max(np.abs(rep.explicit_residual - g["explicit"])) <= HIST_TOL * b0
+    assert d.rank() == int(g["rank"])
+    xh = x.cpu().numpy()
+    _check_x_full(xh[::64], g["x_stride64"])
+    pn = _plane_norms(xh, 200)
+    assert np.max(np.abs(pn - g["x_planes"])) <= X_TOL * np.linalg.norm(g["x_planes"])
+    del xh
+    # (2) m = 100
+    x.zero_()
+    rep = pg.deflated_gmres(dA, b, x, pg.GmresConfig(m=100, max_restarts=2, fixed_iterations=True),
+                            pg.Deflator(pg.DeflationConfig(), ex), ex)
+    assert rep.total_inner == 200 and np.all(np.isfinite(rep.explicit_residual))
+    mon = np.asarray(rep.monitored)
+    for c in range(2):
+        assert abs(mon[100 * c + 99] - rep.explicit_residual[c]) <= 1e-6 * rep.beta0
+    assert rep.explicit_residual[1] < rep.explicit_residual[0] < rep.beta0
