@@ -73,8 +73,9 @@ def metric_name(a):
 def workload(a, n, nnz):
     tag = {125: "BASELINE config 3 (4000x4000-equivalent, largest benchmark mesh)",
            50: "BASELINE config 2 (1000x1000-equivalent)"}.get(a.ne, "custom mesh")
+    nnz_s = f"{nnz:,}" if nnz is not None else "-"
     return {"workload": f"{tag}: 3-D Bratu first Newton system, n_e={a.ne} "
-                        f"({n:,} DOF, {nnz:,} nnz), GMRES({a.m}) + deflation r_max=20, "
+                        f"({n:,} DOF, {nnz_s} nnz), GMRES({a.m}) + deflation r_max=20, "
                         f"rel_tol={a.tol:g}, x0=0",
             "n_e": a.ne, "dof": n, "nnz": nnz, "m": a.m, "rel_tol": a.tol, "r_max": 20,
             "lambda": LAMBDA,
@@ -192,6 +193,7 @@ def run_gpu(a):
     if world > 1:
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines on stderr
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_1906_04051_b200.dgmres import nccl_unique_id
 
@@ -364,7 +366,40 @@ def run_gpu(a):
                "d2h_bytes_per_step": int(8 * n),
                "ms_per_step": round(1e3 * te / a.steps, 3),
                "path": "deflated_gmres(CsrMatrix host arrays, numpy b, x) -> pgm_matrix_upload"
-                       " + pgm_solve(host pointers)"}
+                       " + pgm_solve(host pointers); host arrays pinned"}
+        # the drop-in's real input: pageable host memory (a std::vector in the
+        # reference's CsrMatrix, numpy arrays here)
+        del A_h
+        A_p = pg.CsrMatrix(n, np.array(rp_h.numpy().view(np.uint32)),
+                           np.array(ci_h.numpy().view(np.uint32)), np.array(va_h.numpy()))
+        bp_, xp_ = np.array(bn), np.zeros(n)
+        del rp_h, ci_h, va_h
+
+        def pageable_step():
+            d.reset()
+            xp_[:] = 0.0
+            return pg.deflated_gmres(A_p, bp_, xp_, cfg, d, ex)
+
+        pageable_step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ksteps = max(1, min(a.steps, 3))
+        e0.record(ext)
+        p_iters = 0
+        for _ in range(ksteps):
+            p_iters += pageable_step().total_inner
+        e1.record(ext)
+        torch.cuda.synchronize()
+        tp_ = e0.elapsed_time(e1) / 1e3
+        if dist:
+            tt = torch.tensor([tp_], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tp_ = float(tt.item())
+        e2e["pageable"] = {"value": round(p_iters / tp_, 2), "unit": "iter/s",
+                           "steps": ksteps, "ms_per_step": round(1e3 * tp_ / ksteps, 3),
+                           "path": "same call with pageable numpy arrays"}
+        del A_p
 
     out = {
         "metric": metric_name(a), "value": round(value, 2), "unit": "iter/s",
@@ -432,6 +467,16 @@ def _cpu_model():
 
 
 def run_reference(a):
+    """The reference's own CPU solver (oracle/_ref: its sources compiled
+    verbatim) on this host, all host threads, rank 0 only.  One step = the
+    next restart cycle of ONE deflated GMRES(m) solve of the same system
+    (x and the Deflator carried between steps, refbind.RefSession): the K
+    timed steps are cycles 0..K-1 of the real solve from x0 = 0, so the
+    deflation rank grows 0, 1, 2, ... as in the GPU arm's solve (r <= 20).
+    The W warm-up cycles run first and are then discarded (x, Deflator reset).
+    On n_e <= 50 one step is the complete tolerance solve instead.  A p = 1
+    sample (one fixed cycle from x0 = 0, one thread) is reported beside it
+    (bratu_bench speedup's baseline, bratu_bench.cpp:235-239)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -439,39 +484,94 @@ def run_reference(a):
 
     na = 2 * a.ne + 1
     th = _ref_threads(na)
-    A, b = R.first_newton_system(a.ne, LAMBDA, threads=th)
-    kw = dict(m=a.m, ne=a.ne, threads=th)
-    # bounded sample: one fixed restart cycle (m inner iterations) per step; the
-    # full tolerance solve per step only where it takes seconds (n_e <= 50)
-    if a.ne <= 50:
-        full = R.solve(A, b, max_restarts=100, rel_tol=a.tol, **kw)  # warm-up 0
-        sample = dict(max_restarts=100, rel_tol=a.tol)
-        desc = f"full tolerance solve ({full.total_inner} inner iterations)"
+    t0 = time.perf_counter()
+    S = R.RefSession(a.ne, LAMBDA, threads=th)
+    setup_s = time.perf_counter() - t0
+    nnz = int(S.nnz)
+    full = a.ne <= 50
+    if full:
+        run = lambda: S.run(m=a.m, max_restarts=100, rel_tol=a.tol, fixed_iterations=False)  # noqa: E731
+        desc = "the complete tolerance solve"
     else:
-        sample = dict(max_restarts=1, fixed_iterations=True)
-        desc = f"1 fixed restart cycle ({a.m} inner iterations)"
-        R.solve(A, b, **sample, **kw)  # warm-up 0
-    for _ in range(max(0, a.warmup - 1)):
-        R.solve(A, b, **sample, **kw)
-    iters, secs = 0, 0.0
+        run = lambda: S.run(m=a.m, max_restarts=1, fixed_iterations=True)  # noqa: E731
+        desc = (f"the next restart cycle ({a.m} inner iterations) of one deflated solve "
+                f"from x0 = 0 (timed steps = cycles 0..{a.steps - 1}, deflation rank "
+                f"0..{min(a.steps - 1, 20)})")
+    for _ in range(a.warmup):
+        if full:
+            S.reset()
+        run()
+    S.reset()
+    iters, secs, ranks, rk = 0, 0.0, [], 0
     for _ in range(a.steps):
-        r = R.solve(A, b, **sample, **kw)
+        if full:
+            S.reset()
+            rk = 0
+        ranks.append(rk)  # deflation rank during this step's (first) cycle
+        r = run()
         iters += r.total_inner
         secs += r.wall_s
+        rk = int(r.rank)
     v = iters / secs
+    del S
+    p1 = None
+    # p = 1 costs ~a cycle x the thread count: default on up to n_e = 80
+    # (PGMRES_REF_P1=1 forces it, =0 skips it)
+    p1_mode = os.environ.get("PGMRES_REF_P1", "auto")
+    want_p1 = p1_mode == "1" or (p1_mode == "auto" and a.ne <= 80)
+    if not want_p1:
+        p1 = {"skipped": "p = 1 sample skipped above n_e = 80 to bound the run "
+                         "(PGMRES_REF_P1=1 forces it; profiles/ holds a measured one)"}
+    if want_p1 and th > 1:
+        S1 = R.RefSession(a.ne, LAMBDA, threads=1, assembly_threads=th)
+        r1 = S1.run(m=a.m, max_restarts=1, fixed_iterations=True)
+        p1 = {"value": round(r1.total_inner / r1.wall_s, 4), "unit": "iter/s", "cores": 1,
+              "sample": f"1 fixed restart cycle ({r1.total_inner} inner iterations) from "
+                        f"x0 = 0 (deflation rank 0), {r1.wall_s:.2f} s",
+              "all_cores_speedup": round(v / (r1.total_inner / r1.wall_s), 2)}
+        del S1
     out = {"metric": metric_name(a), "value": round(v, 3), "unit": "iter/s", "n_gpus": a.gpus,
            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 * secs / a.steps, 3),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic: Bratu FEM first Newton system (reference assembly)",
-           "config": workload(a, A.n, A.nnz), "impl": "reference",
+           "config": workload(a, na ** 3, nnz), "impl": "reference",
            "cpu_baseline": {"value": round(v, 3), "unit": "iter/s", "cores": th,
                             "kind": "reference",
-                            "sample": f"{desc} per step, reference deflated_gmres "
-                                      f"(oracle/_ref), deterministic executor, {th} threads",
-                            "cpu_model": _cpu_model()},
+                            "sample": f"{desc} per step; reference deflated_gmres (oracle/_ref), "
+                                      f"deterministic executor, {th} threads; ranks per step "
+                                      f"{ranks}",
+                            "cpu_model": _cpu_model(), "p1": p1,
+                            "setup_s": round(setup_s, 2)},
            "e2e": {"value": round(v, 3), "unit": "iter/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), file=_OUT, flush=True)
+
+
+def self_launch(a) -> int:
+    """`python bench.py --gpus N` outside torchrun: launch N ranks (one process
+    per GPU, torch.distributed.run on 127.0.0.1) and forward rank 0's line."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        print(f"bench.py: --gpus {a.gpus} needs {a.gpus} GPUs, this node has {have}",
+              file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines on stderr
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    res = subprocess.run(cmd, stdout=subprocess.PIPE, text=True, env=env)
+    for ln in res.stdout.splitlines():
+        if ln.startswith("{"):
+            print(ln, file=_OUT, flush=True)
+    return res.returncode
 
 
 def main():
@@ -482,6 +582,8 @@ def main():
     global _OUT
     _OUT = os.fdopen(saved, "w")
     a = parse()
+    if a.impl == "pgmres" and a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(a))
     if a.impl == "reference":
         run_reference(a)
     else:

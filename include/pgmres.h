@@ -204,7 +204,11 @@ uint64_t pgm_context_launch_count(const pgm_context* ctx);
 /* Optional CUDA-event timing of every hot-path kernel of the next solves
  * (class ids: 0 step SpMV, 1 CGS2 pass B (CGS2 step only), 2 DCGS2 update / CGS2
  * pass C, 3 x update,
- * 4 Ritz, 5 push sweeps, 6 push SpMV, 7 rotate, 8 residual, 9 other). */
+ * 4 Ritz, 5 push sweeps, 6 push SpMV, 7 rotate, 8 residual, 9 other;
+ * world > 1: 10 halo planes — the reference Executor's "local" time,
+ * parallel.cpp:249-253 — and 11 NCCL allreduce + replicated finisher — its
+ * "global" time, parallel.cpp:297-300; on the peer transport the allreduce
+ * runs inside the reduction kernels and is not separable). */
 pgm_status pgm_context_set_profiling(pgm_context* ctx, int32_t on);
 uint32_t pgm_context_profile(pgm_context* ctx, uint32_t* cls, uint32_t* cycle, uint32_t* k,
                              float* ms, uint32_t cap);

@@ -303,6 +303,76 @@ int refd_solve(const RefdConfig* c, std::uint32_t n, std::uint64_t nnz,
   }
 }
 
+// ---- resumable deflated solve (bench.py's reference arm) ----------------------
+// The reference solve advanced one call at a time: each refd_session_run is
+// deflated_gmres(A, b, x, cfg, d, ex) with x and the Deflator carried over, so
+// consecutive calls with max_restarts = 1, fixed_iterations = 1 are the
+// consecutive restart cycles of one solve (the per-call beta is the previous
+// cycle's explicit residual, gmres.cpp:141-147,193).  The system, executor and
+// deflator are built once (no per-call CSR copy).
+struct Session {
+  System sys;
+  DenseVector x;
+  std::unique_ptr<Executor> ex;
+  std::unique_ptr<Deflator> d;
+};
+
+void* refd_session_create(void* system, std::uint32_t ne, std::uint32_t threads,
+                          std::uint32_t r_max) {
+  // threads: the solve's executor workers (the system may have been assembled
+  // with another count; assembly is not part of the timed solve)
+  try {
+    auto s = std::make_unique<Session>();
+    s->sys = std::move(*static_cast<System*>(system));
+    s->x.assign(s->sys.jac.n, 0.0);
+    s->ex = make_exec(ne, threads, 1);
+    DeflationConfig dc;
+    dc.r_max = r_max;
+    s->d = std::make_unique<Deflator>(dc);
+    return s.release();
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+int refd_session_run(void* sp, std::uint32_t m, std::uint32_t max_restarts, double rel_tol,
+                     std::int32_t fixed_iterations, RefdReport* rep) {
+  try {
+    Session& s = *static_cast<Session*>(sp);
+    GmresConfig cfg;
+    cfg.m = m;
+    cfg.max_restarts = max_restarts;
+    cfg.rel_tol = rel_tol;
+    cfg.fixed_iterations = fixed_iterations != 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    const GmresReport g = deflated_gmres(s.sys.jac, s.sys.rhs, s.x, cfg, *s.d, *s.ex);
+    const auto t1 = std::chrono::steady_clock::now();
+    std::memset(rep, 0, sizeof(*rep));
+    rep->beta0 = g.beta0;
+    rep->restarts = g.restarts;
+    rep->total_inner = g.total_inner;
+    rep->converged = g.converged;
+    rep->breakdown = g.breakdown;
+    rep->final_relative = g.final_relative;
+    rep->rank = s.d->rank();
+    rep->mu = s.d->mu();
+    rep->skipped = s.d->skipped_updates();
+    rep->wall_s = std::chrono::duration<double>(t1 - t0).count();
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+void refd_session_reset(void* sp) {
+  Session& s = *static_cast<Session*>(sp);
+  std::fill(s.x.begin(), s.x.end(), 0.0);
+  s.d->reset();
+}
+
+void refd_session_free(void* sp) { delete static_cast<Session*>(sp); }
+
 // ---- Deflator unit-level access (test_deflation.cpp patterns) ---------------
 void* refd_deflator_create(std::uint32_t r_max, std::uint32_t drop) {
   try {

@@ -109,6 +109,12 @@ def lib():
                                   C.c_uint32, f64p, C.POINTER(RefdNewtonRec), C.c_uint32,
                                   C.POINTER(C.c_uint32), C.POINTER(C.c_int32),
                                   C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.refd_session_create.restype = C.c_void_p
+        L.refd_session_create.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32]
+        L.refd_session_run.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_double,
+                                       C.c_int32, C.POINTER(RefdReport)]
+        L.refd_session_reset.argtypes = [C.c_void_p]
+        L.refd_session_free.argtypes = [C.c_void_p]
         _lib = L
     return _lib
 
@@ -248,6 +254,43 @@ def solve(A: Csr, b, x0=None, *, m=50, max_restarts=100, rel_tol=1e-8, fixed_ite
         U=U[: n * r].reshape(r, n).T.copy() if (U is not None and r) else None,
         ortho_max=rep.ortho_max, tmatch_max=rep.tmatch_max, rank_max=rep.rank_max,
         wall_s=rep.wall_s)
+
+
+class RefSession:
+    """A reference deflated solve advanced one call at a time (oracle/_ref
+    refd_session_*): run(max_restarts=1, fixed_iterations=True) is the next
+    restart cycle of one solve, x and the Deflator carried over."""
+
+    def __init__(self, ne: int, lam: float = 6.8, threads: int = 0, r_max: int = 20,
+                 assembly_threads: int | None = None):
+        L = lib()
+        h = L.refd_system_create(ne, lam, None,
+                                 threads if assembly_threads is None else assembly_threads)
+        if not h:
+            raise RuntimeError(_err())
+        try:
+            self.n = L.refd_system_n(h)
+            self.nnz = L.refd_system_nnz(h)
+            self.h = L.refd_session_create(h, ne, threads, r_max)
+        finally:
+            L.refd_system_free(h)
+        if not self.h:
+            raise RuntimeError(_err())
+
+    def run(self, m=50, max_restarts=1, rel_tol=1e-10, fixed_iterations=True):
+        rep = RefdReport()
+        if lib().refd_session_run(self.h, m, max_restarts, rel_tol, int(fixed_iterations),
+                                  C.byref(rep)):
+            raise RuntimeError(_err())
+        return rep
+
+    def reset(self):
+        lib().refd_session_reset(self.h)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().refd_session_free(self.h)
+            self.h = None
 
 
 class RefDeflator:

@@ -44,6 +44,9 @@ def _parse(argv):
     ap.add_argument("--reps", type=int, default=3, help="timed repetitions after one warm-up")
     ap.add_argument("--fixed-iterations", action="store_true")
     ap.add_argument("--continuation", action="store_true")
+    ap.add_argument("--loopback", type=int, default=0,
+                    help="speedup only: p = N in-process ranks sharing GPU 0 (host-staged "
+                         "collectives; a one-GPU check of the p > 1 rows)")
     a = ap.parse_args(argv)
     a.ne = [int(v) for v in str(a.ne).split(",") if v]
     for name in ("m", "restarts", "rmax", "reps"):
@@ -99,16 +102,23 @@ def _json_mirror(a, cmd, rows, enabled=True):
         f.write("\n")
 
 
+def _dist_init(local):
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dist
+
+
 def _executor(ne):
     world, rank, local = _world()
     na = 2 * ne + 1
     if world == 1:
         return pg.DeviceExecutor(0), None
     import torch
-    import torch.distributed as dist
 
-    if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = _dist_init(local)
     idt = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
     if rank == 0:
         idt.copy_(torch.frombuffer(bytearray(pg.nccl_unique_id()), dtype=torch.uint8))
@@ -148,56 +158,158 @@ def cmd_convergence(a) -> int:
     return EXIT_OK
 
 
-def cmd_speedup(a) -> int:
-    """cmd_speedup (bratu_bench.cpp:235-329) with p = GPUs: median device time
-    of `reps` fixed-iteration deflated solves after one warm-up, per mesh.
-    compute/local/global percentages from the per-kernel CUDA-event profile
-    (halo exchange = local, allreduce + finisher = global)."""
+PC_HALO, PC_ALLREDUCE = 10, 11  # pgm_context_profile classes (include/pgmres.h)
+
+
+def breakdown(ex, total_s):
+    """TimingBreakdown (parallel.hpp:47-62) of the last solve from the
+    per-launch CUDA-event profile: local = halo planes (class 10, the
+    reference's halo gathers, parallel.cpp:249-253), global = the collective
+    reduction + replicated finisher (class 11, its reductions and barrier
+    waits, parallel.cpp:297-300), compute = the rest of the device time.
+    Returns (compute_s, local_s, global_s)."""
+    cls, _cyc, _k, ms = ex.profile()
+    local = float(ms[cls == PC_HALO].sum()) * 1e-3
+    glob = float(ms[cls == PC_ALLREDUCE].sum()) * 1e-3
+    return max(total_s - local - glob, 0.0), local, glob
+
+
+def _pct(v, parts):
+    t = sum(parts)
+    return 100.0 * v / t if t > 0 else 0.0
+
+
+def _timed_solves(ex, dist, dA, b, cfg, rmax, reps):
+    """One warm-up + `reps` fixed-iteration deflated solves with a fresh
+    Deflator each (bratu_bench.cpp:282-300); the median by device time (max
+    over ranks) and its breakdown."""
     import torch
 
-    world, rank, _ = _world()
-    rows = []
-    for ne in a.ne:
-        ex, dist = _executor(ne)
-        A, b = ex.assemble_bratu(ne, a.lam, device=True)
-        dA = ex.upload(A)
-        cfg = pg.GmresConfig(m=a.m, max_restarts=a.restarts, fixed_iterations=True)
-        d = pg.Deflator(pg.DeflationConfig(r_max=a.rmax), ex)
-        x = torch.zeros(ex.n_own, dtype=torch.float64, device=f"cuda:{ex.device}")
-        samples = []
-        for rep in range(a.reps + 1):
-            d.reset()
+    x = torch.zeros(ex.n_own, dtype=torch.float64, device=f"cuda:{ex.device}")
+    samples = []
+    ex.set_profiling(True)
+    try:
+        for rep in range(reps + 1):
+            d = pg.Deflator(pg.DeflationConfig(r_max=rmax), ex)
             x.zero_()
-            torch.cuda.synchronize()
             r = pg.deflated_gmres(dA, b, x, cfg, d, ex)
+            parts = breakdown(ex, r.solve_seconds)
             t = r.solve_seconds
             if dist is not None:
-                tt = torch.tensor([t], dtype=torch.float64, device=x.device)
+                tt = torch.tensor([t, *parts], dtype=torch.float64, device=x.device)
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                t = float(tt.item())
+                t = float(tt[0].item())
+                # the reference sums its per-worker clocks (parallel.cpp:219-228)
+                ps = torch.tensor(parts, dtype=torch.float64, device=x.device)
+                dist.all_reduce(ps)
+                parts = tuple(float(v) for v in ps.cpu())
             if rep > 0:  # drop the warm-up
-                samples.append(t)
-        samples.sort()
-        med = samples[len(samples) // 2]
-        dof = (2 * ne + 1) ** 3
-        rows.append({"dof": dof, "p": world, "median_s": med, "speedup": 1.0,
-                     "relative_speed": 1.0, "compute_pct": 100.0 if world == 1 else None,
-                     "local_comm_pct": 0.0 if world == 1 else None,
-                     "global_comm_pct": 0.0 if world == 1 else None})
-        del dA, d
-        ex.close()
+                samples.append((t, parts))
+            del d
+    finally:
+        ex.set_profiling(False)
+    samples.sort(key=lambda s: s[0])
+    return samples[len(samples) // 2]
+
+
+def _loopback_solves(ne, world, a, cfg):
+    """The p = world row with `world` in-process ranks on GPU 0 (LoopbackGroup,
+    one host thread per rank, host-staged collectives so the allreduce is
+    timed separately): max over ranks of the device time, summed clocks."""
+    import threading
+
+    os.environ["PGMRES_PEER"] = "0"
+    na = 2 * ne + 1
+    grp = pg.LoopbackGroup(world)
+    out, err = {}, []
+
+    def body(r):
+        try:
+            ex = pg.DeviceExecutor(0, n_global=na ** 3, n_axis=na, rank=r, world=world,
+                                   loopback=grp)
+            A, b = ex.assemble_bratu(ne, a.lam, device=True)
+            dA = ex.upload(A)
+            out[r] = _timed_solves(ex, None, dA, b, cfg, a.rmax, a.reps)
+            del dA
+            ex.close()
+        except Exception as e:  # noqa: BLE001
+            err.append(e)
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    med = max(out[r][0] for r in range(world))
+    parts = tuple(sum(out[r][1][i] for r in range(world)) for i in range(3))
+    return med, parts
+
+
+def cmd_speedup(a) -> int:
+    """cmd_speedup (bratu_bench.cpp:235-329) with p = GPUs.  The p = 1
+    baseline row is always inserted (bratu_bench.cpp:235-239): under torchrun
+    rank 0 first solves alone on its GPU, then all ranks solve the z-slab
+    partitioned system.  Per row: median device time of `reps`
+    fixed-iteration deflated solves after one warm-up, speedup = T1 / Tp,
+    relative_speed = slowest / Tp over the mesh's rows, and the
+    compute / local / global split from the per-kernel profile (breakdown)."""
+    world, rank, local = _world()
+    if a.loopback > 1 and world > 1:
+        raise SystemExit("--loopback runs in one process; do not combine it with torchrun")
+    ps = sorted({1, a.loopback if a.loopback > 1 else world})
+    rows = []
+    for ne in a.ne:
+        cfg = pg.GmresConfig(m=a.m, max_restarts=a.restarts, fixed_iterations=True)
+        first = len(rows)
+        t1 = 0.0
+        for p in ps:
+            if p > 1 and a.loopback > 1:
+                res = _loopback_solves(ne, p, a, cfg)
+            elif p == 1 and world > 1:
+                dist = _dist_init(local)
+                res = None
+                if rank == 0:
+                    ex = pg.DeviceExecutor(local)
+                    A, b = ex.assemble_bratu(ne, a.lam, device=True)
+                    dA = ex.upload(A)
+                    res = _timed_solves(ex, None, dA, b, cfg, a.rmax, a.reps)
+                    del dA
+                    ex.close()
+                dist.barrier()
+            else:
+                ex, dist = _executor(ne)
+                A, b = ex.assemble_bratu(ne, a.lam, device=True)
+                dA = ex.upload(A)
+                res = _timed_solves(ex, dist, dA, b, cfg, a.rmax, a.reps)
+                del dA
+                ex.close()
+            if rank != 0:
+                continue
+            med, parts = res
+            if p == 1:
+                t1 = med
+            rows.append({"dof": (2 * ne + 1) ** 3, "p": p, "median_s": med,
+                         "speedup": t1 / med if t1 > 0 else 1.0, "relative_speed": 1.0,
+                         "compute_pct": _pct(parts[0], parts),
+                         "local_comm_pct": _pct(parts[1], parts),
+                         "global_comm_pct": _pct(parts[2], parts)})
+        if rows[first:]:
+            slowest = max(r["median_s"] for r in rows[first:])
+            for r in rows[first:]:
+                r["relative_speed"] = slowest / r["median_s"]
     lead = rank == 0
     sink = _Sink(a, "speedup", lead)
     sink.write("dof,p,median_s,speedup,relative_speed,compute_pct,local_comm_pct,"
                "global_comm_pct\n")
     for r in rows:
-        pct = ",".join("" if r[k] is None else _g17(r[k])
-                       for k in ("compute_pct", "local_comm_pct", "global_comm_pct"))
         sink.write(f"{r['dof']},{r['p']},{_g17(r['median_s'])},{_g17(r['speedup'])},"
-                   f"{_g17(r['relative_speed'])},{pct}\n")
+                   f"{_g17(r['relative_speed'])},{_g17(r['compute_pct'])},"
+                   f"{_g17(r['local_comm_pct'])},{_g17(r['global_comm_pct'])}\n")
     sink.close()
     _json_mirror(a, "speedup", rows, lead)
-    return EXIT_OK if rows else EXIT_SOLVER_FAILURE
+    return EXIT_OK if (rows or not lead) else EXIT_SOLVER_FAILURE
 
 
 def cmd_solve(a) -> int:

@@ -304,7 +304,11 @@ constexpr int MAX_SPLIT_BLOCKS_PER_SM = 32;  // warp-split CGS2 sweeps (64-128 t
 // Kernel classes of the profile (pgm_context_profile).
 enum ProfClass : uint32_t {
   PC_STEP_SPMV = 0, PC_SWEEP_B = 1, PC_SWEEP_C = 2, PC_XUPDATE = 3, PC_RITZ = 4,
-  PC_PUSH = 5, PC_PUSH_SPMV = 6, PC_ROTATE = 7, PC_RESIDUAL = 8, PC_OTHER = 9
+  PC_PUSH = 5, PC_PUSH_SPMV = 6, PC_ROTATE = 7, PC_RESIDUAL = 8, PC_OTHER = 9,
+  // world > 1: halo planes (NCCL send/recv or loopback copies; the reference's
+  // "local" time) and the collective reduction + replicated finisher (its
+  // "global" time; inside the reduction kernels on the peer transport)
+  PC_HALO = 10, PC_ALLREDUCE = 11
 };
 
 cudaEvent_t prof_event(pgm_context* ctx) {
@@ -318,19 +322,21 @@ cudaEvent_t prof_event(pgm_context* ctx) {
 
 struct ProfScope {
   pgm_context* ctx;
+  cudaStream_t st;
   pgm_context::Rec rec{};
-  ProfScope(pgm_context* c, uint32_t cls, uint32_t k) : ctx(c) {
+  ProfScope(pgm_context* c, uint32_t cls, uint32_t k, cudaStream_t s = nullptr)
+      : ctx(c), st(s ? s : c->stream) {
     if (!ctx->prof_on) return;
     rec.cls = cls;
     rec.cyc = (uint32_t)ctx->prof_cycle;
     rec.k = k;
     rec.a = prof_event(ctx);
     rec.b = prof_event(ctx);
-    cudaEventRecord(rec.a, ctx->stream);
+    cudaEventRecord(rec.a, st);
   }
   ~ProfScope() {
     if (!ctx->prof_on) return;
-    cudaEventRecord(rec.b, ctx->stream);
+    cudaEventRecord(rec.b, st);
     ctx->prof.push_back(rec);
   }
 };
@@ -771,6 +777,7 @@ template <int KIND>
 Status finish_global(pgm_context* ctx, const Params& P, int k, int nv) {
   if (!ctx->coll || ctx->peer) return {};  // peer mode: all-reduced inside the kernel
   if (nv <= 0 || nv > ctx->nvmax) return Status{PGM_ESTATE, "finish_global: bad reduction size"};
+  ProfScope ps(ctx, PC_ALLREDUCE, (uint32_t)k);
   TRY(allreduce_red(ctx, nv));
   k_finish<KIND><<<1, 32, 0, ctx->stream>>>(P, k);
   ctx->launches++;
@@ -1308,6 +1315,7 @@ double* halo_vec(pgm_context* ctx, HaloKind kind, int slot) {
 Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot, cudaStream_t st) {
   if (ctx->world == 1) return {};
   if (!st) st = ctx->stream;
+  ProfScope ps(ctx, PC_HALO, (uint32_t)slot, st);
   double* vec = halo_vec(ctx, kind, slot);
   const size_t lo = ctx->lo, hi = ctx->hi, n = ctx->n;
   const int below = ctx->rank - 1, above = ctx->rank + 1;

@@ -44,16 +44,43 @@ def test_cli_convergence_matches_reference(cuda, ref, tmp_path):
     assert (tmp_path / "conv.json").exists()
 
 
-def test_cli_speedup_schema(cuda):
+def _speedup_rows(argv):
     buf = io.StringIO()
     with redirect_stdout(buf):
-        rc = cli.main(["speedup", "--ne", "6", "--m", "10", "--restarts", "2", "--reps", "2"])
+        rc = cli.main(argv)
     assert rc == 0
     body = [ln for ln in buf.getvalue().splitlines() if not ln.startswith("#")]
     assert body[0] == ("dof,p,median_s,speedup,relative_speed,compute_pct,local_comm_pct,"
                        "global_comm_pct")
-    dof, p, med = body[1].split(",")[:3]
+    return [ln.split(",") for ln in body[1:]]
+
+
+def test_cli_speedup_schema(cuda):
+    rows = _speedup_rows(["speedup", "--ne", "6", "--m", "10", "--restarts", "2", "--reps", "2"])
+    assert len(rows) == 1
+    dof, p, med = rows[0][:3]
     assert int(dof) == 13 ** 3 and int(p) == 1 and float(med) > 0
+    assert float(rows[0][3]) == 1.0 and float(rows[0][5]) == pytest.approx(100.0)
+
+
+def test_cli_speedup_derived_columns(cuda):
+    """test_cli.cpp:225-248 on the GPU: the p = 1 baseline row is inserted,
+    speedup = T1 / Tp, relative_speed = slowest / Tp, and the compute /
+    local / global percentages sum to 100 (p = 2: two in-process ranks on one
+    GPU with host-staged collectives, so the halo and allreduce shares are
+    measured)."""
+    rows = _speedup_rows(["speedup", "--ne", "6", "--m", "10", "--restarts", "2", "--reps", "1",
+                          "--loopback", "2"])
+    assert [r[1] for r in rows] == ["1", "2"]
+    t1, t2 = float(rows[0][2]), float(rows[1][2])
+    slowest = max(t1, t2)
+    for r in rows:
+        med = float(r[2])
+        assert float(r[3]) == pytest.approx(t1 / med, rel=1e-9)
+        assert float(r[4]) == pytest.approx(slowest / med, rel=1e-9)
+        assert float(r[5]) + float(r[6]) + float(r[7]) == pytest.approx(100.0, abs=1e-6)
+    assert float(rows[0][6]) == 0.0 and float(rows[0][7]) == 0.0
+    assert float(rows[1][6]) > 0.0 and float(rows[1][7]) > 0.0
 
 
 def test_cli_solve_writes_solution_and_trace(cuda, tmp_path, golden):

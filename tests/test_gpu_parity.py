@@ -570,7 +570,7 @@ def test_cfg3_deflated_full_size(torch_cuda, golden):
     the reference assembly at u = 0).  The reference run (tests/golden/
     make_golden_large.py, 8 threads, 24 min) gives 24 restarts / 1181 inner
     with truncation active from restart 20; histories within 1e-10 * beta0,
-    solution norm and a strided sample within 1e-8."""
+    the solution (every 16th entry, per-plane norms) within 1e-8."""
     torch = torch_cuda
     g = golden("cfg3_defl")
     ex = pg.DeviceExecutor()
@@ -584,8 +584,13 @@ def test_cfg3_deflated_full_size(torch_cuda, golden):
     xh = x.cpu().numpy()
     xn = float(g["x_norm"])
     assert abs(np.linalg.norm(xh) - xn) <= X_TOL * xn
-    s = int(g["stride"])
-    assert np.linalg.norm(xh[::s] - g["x_sample"]) <= X_TOL * np.linalg.norm(g["x_sample"]) * 10
+    # the solution every 16th entry and its l2 norm on every node plane,
+    # within the north star's 1e-8 (tests/golden/make_golden_r2.py cfg3)
+    gx = golden("cfg3_x")
+    assert int(gx["total_inner"]) == int(g["total_inner"])
+    _check_x_full(xh[::16], gx["x_stride16"])
+    pn = _plane_norms(xh, 125)
+    assert np.max(np.abs(pn - gx["x_planes"])) <= X_TOL * np.linalg.norm(gx["x_planes"])
     assert d.rank() == int(g["rank"])
     hr = np.array([h.r for h in d.history()])
     k = min(len(hr), len(g["hist_r"]))
@@ -615,7 +620,7 @@ def test_restart_length_sweep_ne25(torch_cuda, golden, m, defl):
     assert np.max(np.abs(rep.monitored[:n] - g[key + "_monitored"][:n])) <= HIST_TOL * b0
     xh = x.cpu().numpy()
     assert abs(np.linalg.norm(xh) - float(g[key + "_x_norm"])) <= X_TOL * float(g[key + "_x_norm"])
-    assert np.linalg.norm(xh[::97] - g[key + "_x_sample"]) <= 10 * X_TOL * np.linalg.norm(
+    assert np.linalg.norm(xh[::97] - g[key + "_x_sample"]) <= X_TOL * np.linalg.norm(
         g[key + "_x_sample"])
 
 
