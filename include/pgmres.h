@@ -50,6 +50,8 @@ typedef struct pgm_matrix pgm_matrix;
 typedef struct pgm_deflator pgm_deflator;
 typedef struct pgm_loopback pgm_loopback;
 
+#define PGM_DETERMINISTIC_PLANES 2
+
 /* One rank of a z-slab row-block partition (parallel.cpp:50-71). */
 typedef struct {
   int32_t device;         /* CUDA ordinal this rank drives                   */
@@ -61,7 +63,14 @@ typedef struct {
                           /* when world > 1 (z-slab partition); 0 = no mesh  */
                           /* structure, accepted for world = 1 only          */
   uint32_t n_global;      /* total rows                                      */
-  int32_t deterministic;  /* reserved: reduction order is always fixed       */
+  int32_t deterministic;  /* 0 / 1: reductions in a fixed order (bitwise     */
+                          /* reproducible run to run for a given partition); */
+                          /* PGM_DETERMINISTIC_PLANES: every reduction is    */
+                          /* per-plane sequential partials + the reference's */
+                          /* pairwise fold (parallel.cpp:33-46,120-131) —    */
+                          /* bit-identical for ANY rank count (and equal to  */
+                          /* the reference executor's dot); slower; no peer  */
+                          /* transport                                       */
 } pgm_context_config;
 
 typedef struct {

@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -438,7 +439,11 @@ int refd_newton(std::uint32_t ne, double lambda, std::uint32_t max_iters, double
                 std::int32_t* converged, double* final_residual, double* wall_s) {
   try {
     const StructuredMesh mesh = build_mesh(ne);
-    auto ex = make_exec(ne, threads, 1);
+    // REFD_EXEC=nondet: the reference's non-deterministic executor (per-worker
+    // partials) — used to measure the reference's own run-to-run spread
+    const char* ev = std::getenv("REFD_EXEC");
+    const int det = (ev && std::string(ev) == "nondet") ? 0 : 1;
+    auto ex = make_exec(ne, threads, det);
     NewtonConfig cfg;
     cfg.max_iters = max_iters;
     cfg.update_tol = update_tol;

@@ -46,5 +46,24 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """A tuning variant (e.g. -DPGM_TILE=256) at _lib/variants/libpgmres_<name>.so,
+    selected at run time with PGMRES_LIB=<path> (paper_1906_04051_b200/_capi.py)."""
+    out = os.path.join(LIBDIR, "variants", f"libpgmres_{name}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [NVCC, *ARCH, *FLAGS, *defines, "-o", out, os.path.join(CSRC, "pgmres.cu"), "-ldl"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stderr[-8000:])
+    with open(out + ".ptxas.log", "w") as f:
+        f.write(res.stderr)
+    return out
+
+
 if __name__ == "__main__":
-    print(build_library(force=True))
+    import sys
+
+    if len(sys.argv) > 2 and sys.argv[1] == "variant":
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        print(build_library(force=True))

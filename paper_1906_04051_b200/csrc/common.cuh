@@ -90,7 +90,7 @@ struct Params {
   size_t ld;
   int n, lo, m, R1;
   // reduction scratch
-  double *part, *gpart;
+  double *part, *gpart, *g2part;
   unsigned* cnt;
   double* red_out;  // world > 1: block-reduced local sums for the allreduce
   int world;
@@ -103,6 +103,16 @@ struct Params {
   const double* win_local;
   const unsigned long long* flag_local;
   unsigned long long* epoch;                // this rank's reduction counter
+  // deterministic mode (pgm_context_config.deterministic = 2): every
+  // reduction is recomputed as per-plane sequential partials + the
+  // reference's pairwise fold (k_det_dots), bit-identical for any rank count
+  int det;
+  int plane;            // rows per node plane (n_axis^2; n for world = 1 without mesh)
+  int nplanes;          // this rank's planes
+  double* det_pp;       // [nv][nplanes] this rank's plane partials
+  const double* det_all;  // world > 1: [nv][nplanes_global] gathered partials
+  int nplanes_global;
+  unsigned* det_cnt;    // completion counter of k_det_dots
 };
 
 constexpr int PEER_NV = 2 * MAX_R1 + MAX_M + 8;  // values per reduction slot
@@ -155,9 +165,24 @@ constexpr int VPW = PGM_VPW;
 // reduction may span several launches, e.g. the interior and boundary tiles
 // of a halo-overlapped SpMV; partials are indexed by tile, so the order is
 // the same however the launches interleave).
+#ifndef PGM_TAIL_TIMING
+#define PGM_TAIL_TIMING 0  // tuning variant: %globaltimer stamps of the reduction tail
+#endif
+#if PGM_TAIL_TIMING
+__device__ unsigned long long g_tail_ns[8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__shared__ unsigned long long s_tail_t[3];
+#endif
 __device__ __forceinline__ bool grid_reduce_ex(const double* bvals, int nv, const Params& P,
                                                double* red, int G, int bid) {
   __shared__ int s_flag;
+#if PGM_TAIL_TIMING
+  if (threadIdx.x == 0) s_tail_t[0] = gtimer();
+#endif
   const int NG = (G + GROUP - 1) / GROUP;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int v = threadIdx.x; v < nv; v += blockDim.x) P.part[(size_t)v * G + bid] = bvals[v];
@@ -192,23 +217,64 @@ __device__ __forceinline__ bool grid_reduce_ex(const double* bvals, int nv, cons
   if (threadIdx.x == 0) P.cnt[1 + grp] = 0;
   __threadfence();
   __syncthreads();
+  // level 2: with more than GROUP groups, super-groups of GROUP groups are
+  // summed by their last group-reducer (distributed), so the final block
+  // reads at most GROUP partials per value (a single block walking ~1000
+  // groups per value was ~25 us of the step at n_e = 125)
+  const int NS = (NG + GROUP - 1) / GROUP;
+  const double* lvl = P.gpart;
+  int nlvl = NG;
+  if (NS > 1) {
+    const int sg = grp / GROUP, s0 = sg * GROUP, ssize = min(GROUP, NG - s0);
+    if (threadIdx.x == 0) {
+      const unsigned t = atomicAdd(&P.cnt[1 + NG + sg], 1u);
+      s_flag = (t == (unsigned)(ssize - 1));
+    }
+    __syncthreads();
+    if (!s_flag) return false;
+    __threadfence();
+    for (int v0 = warp * VPW; v0 < nv; v0 += nw * VPW) {
+      double s[VPW];
+#pragma unroll
+      for (int q = 0; q < VPW; ++q)
+        s[q] = (v0 + q < nv && lane < ssize) ? __ldcg(&P.gpart[(size_t)(v0 + q) * NG + s0 + lane]) : 0.0;
+#pragma unroll
+      for (int q = 0; q < VPW; ++q) s[q] = warp_sum(s[q]);
+      if (lane < VPW && v0 + lane < nv) {
+        double o = s[0];
+#pragma unroll
+        for (int q = 1; q < VPW; ++q)
+          if (lane == q) o = s[q];
+        P.g2part[(size_t)(v0 + lane) * NS + sg] = o;
+      }
+    }
+    if (threadIdx.x == 0) P.cnt[1 + NG + sg] = 0;
+    __threadfence();
+    __syncthreads();
+    lvl = P.g2part;
+    nlvl = NS;
+  }
   if (threadIdx.x == 0) {
     const unsigned t = atomicAdd(&P.cnt[0], 1u);
-    s_flag = (t == (unsigned)(NG - 1));
+    s_flag = (t == (unsigned)((NS > 1 ? NS : NG) - 1));
   }
   __syncthreads();
   if (!s_flag) return false;
   __threadfence();
-  // level 2: lanes stride over the groups, VPW values per warp pass
+#if PGM_TAIL_TIMING
+  if (threadIdx.x == 0) s_tail_t[1] = gtimer();
+#endif
+  // final level: lanes stride over the partials, VPW values per warp pass
   for (int v0 = warp * VPW; v0 < nv; v0 += nw * VPW) {
     double s[VPW];
 #pragma unroll
     for (int q = 0; q < VPW; ++q) s[q] = 0.0;
-    for (int g = lane; g < NG; g += 32) {
+#pragma unroll 4
+    for (int g = lane; g < nlvl; g += 32) {
       double t[VPW];
 #pragma unroll
       for (int q = 0; q < VPW; ++q)
-        t[q] = v0 + q < nv ? __ldcg(&P.gpart[(size_t)(v0 + q) * NG + g]) : 0.0;
+        t[q] = v0 + q < nv ? __ldcg(&lvl[(size_t)(v0 + q) * nlvl + g]) : 0.0;
 #pragma unroll
       for (int q = 0; q < VPW; ++q) s[q] += t[q];
     }
@@ -223,6 +289,9 @@ __device__ __forceinline__ bool grid_reduce_ex(const double* bvals, int nv, cons
     }
   }
   if (threadIdx.x == 0) P.cnt[0] = 0;
+#if PGM_TAIL_TIMING
+  if (threadIdx.x == 0) s_tail_t[2] = gtimer();
+#endif
   __syncthreads();
   return true;
 }
@@ -320,6 +389,7 @@ __device__ __forceinline__ void peer_allreduce(double* red, int nv, const Params
 // Returns true in the block that must run the finisher on red.
 __device__ __forceinline__ bool reduce_tail(const double* bvals, int nv, const Params& P,
                                             double* red, int G, int bid) {
+  if (P.det) return false;  // k_det_dots recomputes this reduction and finishes it
   if (!grid_reduce_ex(bvals, nv, P, red, G, bid)) return false;
   if (P.world > 1 && !P.peer) {
     for (int v = threadIdx.x; v < nv; v += blockDim.x) P.red_out[v] = red[v];

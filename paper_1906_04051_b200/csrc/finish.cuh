@@ -26,12 +26,17 @@ __device__ __forceinline__ void defl_coeffs(const Params& P, int r, const double
 }
 
 // Block-collective version (t must be visible to every thread of the block).
-__device__ __forceinline__ void defl_coeffs_par(const Params& P, int r, const double* t,
-                                                double* c) {
+__device__ __forceinline__ void defl_coeffs_par(const Params& P, int r,
+                                                const double* __restrict__ t,
+                                                double* __restrict__ c) {
   const double amu = fabs(P.d->mu);
+  const double* __restrict__ ti = P.Tinv;
+  const int R1 = P.R1;
   for (int i = threadIdx.x; i < r; i += blockDim.x) {
     double s = 0.0;
-    for (int j = 0; j < r; ++j) s += P.Tinv[i + j * P.R1] * t[j];
+    // independent loads batched (the finisher is on the step's critical path)
+#pragma unroll 8
+    for (int j = 0; j < r; ++j) s += ti[i + j * R1] * t[j];
     c[i] = amu * s - t[i];
   }
 }
@@ -253,90 +258,129 @@ __device__ void fin_sweep_b(const Params& P, int k, const double* red) {
 // coefB[l] = -(Ha_l/beta + h1_l) s_l (l < k), coefB[k] = -(Ha_k/beta + h1_k) s_k.
 // tU[k] holds U^T u_k (raw) until the step finalises it.
 
-// Column k-1 completion (thread 0; sa = a from smem).  Returns 1 to continue.
+// Column k-1 completion, called by EVERY thread of the finishing block (sa = a
+// in smem).  The global reads (column k-1 of H, the previous rotations) are
+// issued block-parallel into smem first; thread 0 then runs the short serial
+// part (Givens chain, records, exits) on smem only — the finisher sits on
+// the critical path between two kernels, so its latency chain matters.
+// Returns 1 (in every thread) to continue.
 __device__ int dcgs2_column(const Params& P, int k, const double* sa, double alpha, bool close,
                             double* sH, double* s_beta) {
+  __shared__ double sC[MAX_M], sS[MAX_M], s_na2;
+  __shared__ int s_ret;
   GState* g = P.g;
   const int m = P.m;
   const size_t col = (size_t)(k - 1) * (m + 1);
-  double na2 = 0.0;
-  for (int l = 0; l < k; ++l) na2 += sa[l] * sa[l];
-  // Pythagorean remainder ||u_k - Q a||^2 = alpha - ||a||^2.  When it sits at
-  // rounding level of alpha the value carries no digits (it can even clamp to
-  // 0).  If the bound sqrt(floor) is itself below the breakdown threshold the
-  // Krylov space is exhausted (gmres.cpp:173 fires for any true value);
-  // otherwise the step is ambiguous: the cycle closes here (not a lucky
-  // breakdown) and later cycles run the CGS2 step, whose remainder norm is
-  // formed explicitly (pass B) — no false breakdown at the rounding floor.
-  const double diff = alpha - na2;
-  const double floor2 = 4.0 * (k + 1) * 2.220446049250313e-16 * alpha;
-  bool ambiguous = false;
-  double beta = sqrt(fmax(diff, 0.0));
-  if (diff <= floor2 && alpha > 0.0 && sqrt(floor2) >= g->breakdown_scale * g->beta_cycle) {
-    ambiguous = true;
-    beta = sqrt(floor2);
+  const int kk = k - 1;  // the column being completed
+  // thread 0's scalars, loaded up front (they land during the parallel phase)
+  double bscale = 0.0, bcyc = 0.0, gk = 0.0, rtol = 0.0, b0 = 0.0;
+  int fixed = 0, restart = 0, ninner = 0;
+  if (threadIdx.x == 0) {
+    bscale = g->breakdown_scale;
+    bcyc = g->beta_cycle;
+    gk = P.gv[kk];
+    rtol = g->rel_tol;
+    b0 = g->beta0;
+    fixed = g->fixed;
+    restart = g->restart;
+    ninner = g->n_inner;
   }
-  *s_beta = beta;
-  for (int l = 0; l < k; ++l) {
+  for (int l = threadIdx.x; l < k; l += blockDim.x) {
     const double h = P.h_orig[col + l] + sa[l];
     P.h_orig[col + l] = h;
     sH[l] = h;
+    if (l < kk) {
+      sC[l] = P.cs[l];
+      sS[l] = P.sn[l];
+    }
   }
-  sH[k] = beta;
-  P.h_orig[col + k] = beta;
-  if (!isfinite(beta) || !isfinite(alpha)) {
-    set_error(P, 2, g->restart, k - 1);
-    return 0;
+  if (threadIdx.x < 32) {
+    double v = 0.0;
+    for (int l = threadIdx.x; l < k; l += 32) v += sa[l] * sa[l];
+    v = warp_sum(v);
+    if (threadIdx.x == 0) s_na2 = v;
   }
-  const int kk = k - 1;  // the column being completed
-  for (int i = 0; i < kk; ++i) {
-    const double hi = sH[i], hj = sH[i + 1];
-    sH[i] = P.cs[i] * hi + P.sn[i] * hj;
-    sH[i + 1] = -P.sn[i] * hi + P.cs[i] * hj;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_ret = 0;
+    const double na2 = s_na2;
+    // Pythagorean remainder ||u_k - Q a||^2 = alpha - ||a||^2.  When it sits at
+    // rounding level of alpha the value carries no digits (it can even clamp
+    // to 0).  If the bound sqrt(floor) is itself below the breakdown
+    // threshold the Krylov space is exhausted (gmres.cpp:173 fires for any
+    // true value); otherwise the step is ambiguous: the cycle closes here (not
+    // a lucky breakdown) and later cycles run the CGS2 step, whose remainder
+    // norm is formed explicitly (pass B) — no false breakdown at the rounding
+    // floor.
+    const double diff = alpha - na2;
+    const double floor2 = 4.0 * (k + 1) * 2.220446049250313e-16 * alpha;
+    bool ambiguous = false;
+    double beta = sqrt(fmax(diff, 0.0));
+    if (diff <= floor2 && alpha > 0.0 && sqrt(floor2) >= bscale * bcyc) {
+      ambiguous = true;
+      beta = sqrt(floor2);
+    }
+    *s_beta = beta;
+    sH[k] = beta;
+    P.h_orig[col + k] = beta;
+    if (!isfinite(beta) || !isfinite(alpha)) {
+      set_error(P, 2, restart, k - 1);
+    } else {
+      for (int i = 0; i < kk; ++i) {
+        const double hi = sH[i], hj = sH[i + 1];
+        sH[i] = sC[i] * hi + sS[i] * hj;
+        sH[i + 1] = -sS[i] * hi + sC[i] * hj;
+      }
+      const double a = sH[kk], b = sH[kk + 1];
+      const double rr = hypot(a, b);
+      double ck, sk;
+      if (rr == 0.0) {
+        ck = 1.0;
+        sk = 0.0;
+      } else {
+        ck = a / rr;
+        sk = b / rr;
+      }
+      P.cs[kk] = ck;
+      P.sn[kk] = sk;
+      sH[kk] = rr;
+      sH[kk + 1] = 0.0;
+      P.gv[kk + 1] = -sk * gk;
+      P.gv[kk] = ck * gk;
+      const double monitored = fabs(-sk * gk);
+      const int idx = ninner;
+      g->n_inner = ninner + 1;
+      P.rec_restart[idx] = (uint32_t)restart;
+      P.rec_step[idx] = (uint32_t)kk;
+      P.rec_mon[idx] = monitored;
+      g->steps = kk + 1;
+      bool stop = close || kk + 1 >= m;
+      if (ambiguous) {
+        g->dc_fallback = 1;
+        stop = true;
+      } else if (beta < bscale * bcyc) {
+        g->lucky = 1;
+        stop = true;
+      } else if (!fixed && monitored <= rtol * b0) {
+        stop = true;
+      }
+      if (stop) {
+        g->active = 0;
+      } else {
+        // beta == 0 without the breakdown exit (breakdown_scale = 0 or
+        // beta_cycle = 0, fixed iterations): continue with finite
+        // coefficients, as the reference's arnoldi_step does for hnext == 0
+        // (gmres.cpp:60-63)
+        P.s[k] = beta > 0.0 ? 1.0 / beta : 0.0;
+        s_ret = 1;
+      }
+    }
   }
-  const double a = sH[kk], b = sH[kk + 1];
-  const double rr = hypot(a, b);
-  double ck, sk;
-  if (rr == 0.0) {
-    ck = 1.0;
-    sk = 0.0;
-  } else {
-    ck = a / rr;
-    sk = b / rr;
-  }
-  P.cs[kk] = ck;
-  P.sn[kk] = sk;
-  sH[kk] = rr;
-  sH[kk + 1] = 0.0;
-  for (int i = 0; i <= kk + 1; ++i) P.h_rot[col + i] = sH[i];
-  const double gk = P.gv[kk];
-  P.gv[kk + 1] = -sk * gk;
-  P.gv[kk] = ck * gk;
-  const double monitored = fabs(-sk * gk);
-  const int idx = g->n_inner++;
-  P.rec_restart[idx] = (uint32_t)g->restart;
-  P.rec_step[idx] = (uint32_t)kk;
-  P.rec_mon[idx] = monitored;
-  g->steps = kk + 1;
-  bool stop = close || kk + 1 >= m;
-  if (ambiguous) {
-    g->dc_fallback = 1;
-    stop = true;
-  } else if (beta < g->breakdown_scale * g->beta_cycle) {
-    g->lucky = 1;
-    stop = true;
-  } else if (!g->fixed && monitored <= g->rel_tol * g->beta0) {
-    stop = true;
-  }
-  if (stop) {
-    g->active = 0;
-    return 0;
-  }
-  // beta == 0 without the breakdown exit (breakdown_scale = 0 or beta_cycle
-  // = 0, fixed iterations): continue with finite coefficients, as the
-  // reference's arnoldi_step does for hnext == 0 (gmres.cpp:60-63)
-  P.s[k] = beta > 0.0 ? 1.0 / beta : 0.0;
-  return 1;
+  __syncthreads();
+  // the rotated column (h_rot, gmres.cpp:67-90), written block-parallel
+  if (isfinite(*s_beta))
+    for (int i = threadIdx.x; i <= kk + 1; i += blockDim.x) P.h_rot[col + i] = sH[i];
+  return s_ret;
 }
 
 __device__ void fin_dcgs2(const Params& P, int k, const double* red) {
@@ -354,13 +398,14 @@ __device__ void fin_dcgs2(const Params& P, int k, const double* red) {
     if (l < k) sa[l] = sl * red[nb + l];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (k == 0) {
+  if (k == 0) {
+    if (threadIdx.x == 0) {
       s_go = 1;
       s_beta = 1.0;
-    } else {
-      s_go = dcgs2_column(P, k, sa, alpha, false, sH, (double*)&s_beta);
     }
+  } else {
+    const int go = dcgs2_column(P, k, sa, alpha, false, sH, (double*)&s_beta);
+    if (threadIdx.x == 0) s_go = go;
   }
   __syncthreads();
   if (!s_go) return;
@@ -385,8 +430,11 @@ __device__ void fin_dcgs2(const Params& P, int k, const double* red) {
   }
   // H[:k+1, :k] a (Hessenberg: row l has columns >= l-1)
   for (int l = threadIdx.x; l <= k; l += blockDim.x) {
+    // independent loads batched 8 deep (no stores in the loop)
+    const double* __restrict__ hrow = P.h_orig + l;
     double s = 0.0;
-    for (int j = (l > 0 ? l - 1 : 0); j < k; ++j) s += P.h_orig[(size_t)j * (m + 1) + l] * sa[j];
+#pragma unroll 8
+    for (int j = (l > 0 ? l - 1 : 0); j < k; ++j) s += __ldcg(hrow + (size_t)j * (m + 1)) * sa[j];
     sHa[l] = s;
   }
   if (threadIdx.x == 0) {
@@ -415,12 +463,17 @@ __device__ void fin_dcgs2(const Params& P, int k, const double* red) {
   double* tk = P.tU + (size_t)k * R1;
   double* tn = P.tU + (size_t)(k + 1) * R1;
   for (int j = threadIdx.x; j < r; j += blockDim.x) {
-    double t = tk[j];
-    for (int l = 0; l < k; ++l) t -= sa[l] * P.tU[(size_t)l * R1 + j];
+    // one pass over U^T v_l (global, loads batched 8 deep) for both sums
+    const double* __restrict__ tcol = P.tU + j;
+    double t = tk[j], u = Uy[j] * ib;
+#pragma unroll 8
+    for (int l = 0; l < k; ++l) {
+      const double tl = __ldcg(tcol + (size_t)l * R1);
+      t -= sa[l] * tl;
+      u -= (sHa[l] * ib + sh1[l]) * tl;
+    }
     const double tq = sk * t;
     tk[j] = tq;
-    double u = Uy[j] * ib;
-    for (int l = 0; l < k; ++l) u -= (sHa[l] * ib + sh1[l]) * P.tU[(size_t)l * R1 + j];
     u -= (sHa[k] * ib + sh1[k]) * tq;
     tn[j] = u;
   }
@@ -436,8 +489,7 @@ __device__ void fin_dcgs2_close(const Params& P, const double* red) {
   const int m = P.m;
   for (int l = threadIdx.x; l < m; l += blockDim.x) sa[l] = P.s[l] * red[l];
   __syncthreads();
-  if (threadIdx.x == 0) dcgs2_column(P, m, sa, red[m], true, sH, (double*)&s_beta);
-  __syncthreads();
+  dcgs2_column(P, m, sa, red[m], true, sH, (double*)&s_beta);
 }
 
 // ---- restart harvest: push_vector (deflation.cpp:123-184) ----------------------

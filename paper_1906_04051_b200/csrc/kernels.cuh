@@ -528,7 +528,19 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
     pdl_trigger();
     __syncthreads();
     const int G = SEG ? A.ntiles : (int)gridDim.x;
-    if (reduce_tail(bvals, nv, P, red, G, tile)) E.finish(P, red);
+    if (reduce_tail(bvals, nv, P, red, G, tile)) {
+      E.finish(P, red);
+#if PGM_TAIL_TIMING
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned long long t3 = gtimer();
+        atomicAdd(&g_tail_ns[0], s_tail_t[1] - s_tail_t[0]);  // level-1 chain (final block)
+        atomicAdd(&g_tail_ns[1], s_tail_t[2] - s_tail_t[1]);  // level 2
+        atomicAdd(&g_tail_ns[2], t3 - s_tail_t[2]);           // finisher
+        atomicAdd(&g_tail_ns[3], 1ull);
+      }
+#endif
+    }
     return;
   }
   if constexpr (std::is_same<Epi, StepEpi>::value) {
@@ -1213,6 +1225,174 @@ __global__ void k_finish(Params P, int k) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Deterministic mode: every reduction value is dot(a_v, b_v) over the owned
+// rows of two vectors that the reduction kernel left in memory.  k_det_dots
+// forms, per node plane, the sequential sum  acc += a_i * b_i  over the
+// plane's rows in ascending order (the reference's deterministic
+// Executor::dot_kernel with block = n_axis^2, parallel.cpp:120-131), then
+// combines the planes with the reference's pairwise fold (parallel.cpp:33-46)
+// — for one rank in the kernel's last block, for world > 1 after the plane
+// partials of all ranks were gathered (k_det_finish).  The result depends
+// only on the vectors, never on the partition: bit-identical for any rank
+// count, and bit-identical to the reference executor's dot of the same
+// vectors.  The finishers then run unchanged (same dispatch as k_finish).
+struct DetPair {
+  const double* a;
+  const double* b;
+};
+
+template <int KIND>
+__device__ __forceinline__ bool det_skip(const Params& P, int k) {
+  if (KIND == 100 || KIND == 103) return !P.g->active;
+  if (KIND == 101) return P.g->error != 0 || (!k && P.g->done);
+  if (KIND == 102) return !P.d->push_ok;
+  if (KIND == SW_CGS2_B) return !P.g->active;
+  return sweep_spec<KIND>(P, k).skip != 0;
+}
+
+template <int KIND>
+__device__ __forceinline__ int det_nv(const Params& P, int k) {
+  const int r = P.d->r;
+  if (KIND == 100) return k + 1;
+  if (KIND == 101) return 1 + r;
+  if (KIND == 102) return 2 * r + 1;
+  if (KIND == 103) return (k > 0 ? k : 1) + k + 2 + r;
+  if (KIND == SW_CGS2_B) return k + 2 + r;
+  const SweepSpec S = sweep_spec<KIND>(P, k);
+  return S.nq + (S.selfnorm ? 1 : 0);
+}
+
+template <int KIND>
+__device__ __forceinline__ DetPair det_pair(const Params& P, int k, int v) {
+  const size_t ld = P.ld, lo = P.lo;
+  const double* V = P.V + lo;
+  const double* U = P.U + lo;
+  const double* AU = P.AU + lo;
+  if (KIND == 100) return {V + (size_t)v * ld, V + (size_t)(k + 1) * ld};
+  if (KIND == 101) return v == 0 ? DetPair{V, V} : DetPair{U + (size_t)(v - 1) * ld, V};
+  if (KIND == 102) {
+    const int j = P.d->r;
+    if (v < j) return {U + (size_t)v * ld, AU + (size_t)j * ld};
+    if (v == j) return {U + (size_t)j * ld, AU + (size_t)j * ld};
+    return {U + (size_t)j * ld, AU + (size_t)(v - j - 1) * ld};
+  }
+  if (KIND == 103) {
+    const int nb = k > 0 ? k : 1;
+    const double* y = V + (size_t)(k + 1) * ld;
+    const double* u = V + (size_t)k * ld;
+    if (v < nb) return {V + (size_t)v * ld, y};
+    if (v < nb + k) return {V + (size_t)(v - nb) * ld, u};
+    if (v == nb + k) return {u, u};
+    if (v == nb + k + 1) return {u, y};
+    return {U + (size_t)(v - nb - k - 2) * ld, y};
+  }
+  if (KIND == SW_CGS2_B) {
+    const double* w = V + (size_t)(k + 1) * ld;
+    if (v <= k) return {V + (size_t)v * ld, w};
+    if (v == k + 1) return {w, w};
+    return {U + (size_t)(v - k - 2) * ld, w};
+  }
+  const SweepSpec S = sweep_spec<KIND>(P, k);
+  const double* o = S.out;
+  if (S.selfnorm) {
+    const int self = S.normlast ? S.nq : 0;
+    if (v == self) return {o, o};
+    const int q = S.normlast ? v : v - 1;
+    return {S.Q + (size_t)q * ld, o};
+  }
+  return {S.Q + (size_t)v * ld, o};
+}
+
+// the reference's pairwise fold over s[0..n) (destroys s)
+__device__ __forceinline__ double det_fold(double* s, int n) {
+  if (n == 0) return 0.0;
+  while (n > 1) {
+    const int m = n / 2;
+    for (int i = 0; i < m; ++i) s[i] = __dadd_rn(s[2 * i], s[2 * i + 1]);
+    int nm = m;
+    if (n % 2) s[nm++] = s[n - 1];
+    n = nm;
+  }
+  return s[0];
+}
+
+template <int KIND>
+__device__ __forceinline__ void det_finish_dispatch(const Params& P, int k, const double* red) {
+  if (KIND == 100) {
+    fin_step_spmv(P, k, red);
+  } else if (KIND == 101) {
+    fin_residual(P, red, k != 0);
+  } else if (KIND == 102) {
+    if (threadIdx.x == 0) fin_push_spmv(P, red);
+  } else if (KIND == 103) {
+    fin_dcgs2(P, k, red);
+  } else {
+    sweep_finish<KIND>(P, k, red);
+  }
+}
+
+constexpr int DET_THREADS = 128;
+constexpr int DET_MAXNV = 2 * MAX_M + 2 + MAX_R1;
+
+// One thread per (plane, value): the sequential plane sum.  Launched after
+// the reduction kernel (stream order), grid = ceil(nplanes * nv / 128).
+template <int KIND>
+__global__ void __launch_bounds__(DET_THREADS) k_det_dots(Params P, int k) {
+  __shared__ double red[DET_MAXNV];
+  __shared__ int s_last;
+  if (det_skip<KIND>(P, k)) return;
+  const int nv = det_nv<KIND>(P, k);
+  const int np = P.nplanes;
+  const long t = (long)blockIdx.x * DET_THREADS + threadIdx.x;
+  if (t < (long)np * nv) {
+    const int q = (int)(t / nv), v = (int)(t % nv);
+    const DetPair pr = det_pair<KIND>(P, k, v);
+    const long r0 = (long)q * P.plane;
+    const int rows = (int)min((long)P.plane, (long)P.n - r0);
+    const double* a = pr.a + r0;
+    const double* b = pr.b + r0;
+    double acc = 0.0;
+    int i = 0;
+    for (; i + 4 <= rows; i += 4) {  // loads run ahead of the (sequential) sum
+      const double a0 = a[i], a1 = a[i + 1], a2 = a[i + 2], a3 = a[i + 3];
+      const double b0 = b[i], b1 = b[i + 1], b2 = b[i + 2], b3 = b[i + 3];
+      acc = __dadd_rn(acc, __dmul_rn(a0, b0));
+      acc = __dadd_rn(acc, __dmul_rn(a1, b1));
+      acc = __dadd_rn(acc, __dmul_rn(a2, b2));
+      acc = __dadd_rn(acc, __dmul_rn(a3, b3));
+    }
+    for (; i < rows; ++i) acc = __dadd_rn(acc, __dmul_rn(a[i], b[i]));
+    P.det_pp[(size_t)v * np + q] = acc;
+  }
+  if (P.world > 1) return;  // gathered on the host side, folded by k_det_finish
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(P.det_cnt, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int v = threadIdx.x; v < nv; v += DET_THREADS)
+    red[v] = det_fold(P.det_pp + (size_t)v * np, np);
+  if (threadIdx.x == 0) *P.det_cnt = 0;
+  __syncthreads();
+  det_finish_dispatch<KIND>(P, k, red);
+}
+
+// world > 1: fold the gathered plane partials of all ranks (global plane
+// order) and run the finisher, identically on every rank.
+template <int KIND>
+__global__ void __launch_bounds__(DET_THREADS) k_det_finish(Params P, int k) {
+  __shared__ double red[DET_MAXNV];
+  if (det_skip<KIND>(P, k)) return;
+  const int nv = det_nv<KIND>(P, k);
+  const int npg = P.nplanes_global;
+  double* all = const_cast<double*>(P.det_all);
+  for (int v = threadIdx.x; v < nv; v += DET_THREADS) red[v] = det_fold(all + (size_t)v * npg, npg);
+  __syncthreads();
+  det_finish_dispatch<KIND>(P, k, red);
+}
+
 // End of an Arnoldi cycle (the inner loop stopped in fin_sweep_c): back-
 // substitution of the rotated Hessenberg system (solve_least_squares,
 // gmres.cpp:92-107; same row-oriented summation order, from a shared-memory
@@ -1326,51 +1506,55 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
     return;
   }
   const double tol = d->inv_tol;
-  // ---- largest_ritz_value: power iteration (deflation.cpp:57-82); block
-  // sums with one barrier each (separate slot arrays per sum).
-  __shared__ double sA[RITZ_THREADS / 32], sB[RITZ_THREADS / 32];
-  auto bsum1 = [&](double v, double* slots) {
-    v = warp_sum(v);
-    if ((tid & 31) == 0) slots[tid >> 5] = v;
-    __syncthreads();
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += slots[w];
-    return t;
+  const int warp = tid >> 5, lane = tid & 31;
+  // H (Hessenberg block, column-major i + j (m+1)) read by lane-per-row
+  // matvecs straight from P.h_orig (L1-resident after the first sweep): the
+  // smem copy is consumed by the Gauss-Jordan inverse that runs meanwhile.
+  const double* hg = P.h_orig;
+  const size_t hld = (size_t)m + 1;
+  constexpr int RQ = (MAX_M + 31) / 32;  // rows per lane
+  auto hmv_global = [&](const double* v, double (&out)[RQ]) {
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) {
+      const int i = lane + 32 * q;
+      double s0 = 0.0, s1 = 0.0;
+      if (i < k) {
+        int j = i > 0 ? i - 1 : 0;  // Hessenberg: H(i, j) = 0 for j < i - 1
+        for (; j + 1 < k; j += 2) {
+          s0 += __ldg(hg + (size_t)j * hld + i) * v[j];
+          s1 += __ldg(hg + (size_t)(j + 1) * hld + i) * v[j + 1];
+        }
+        if (j < k) s0 += __ldg(hg + (size_t)j * hld + i) * v[j];
+      }
+      out[q] = s0 + s1;
+    }
   };
-  {
-    // y = H z_{i-1} (unnormalised iterate), hy = H y.  One fused sum gives
-    // y.y and y.hy (nz = |y|, theta = y.hy / y.y = z.Hz), the second
-    // |hy - theta y|^2 / y.y (= |Hz - theta z|^2) while y <- hy / nz is
-    // written for the next iteration: 3 barriers and 2 reductions per step.
-    __shared__ double sA2[RITZ_THREADS / 32];
-    double* y = nx;
-    double* hy = hz;
-    for (int i = tid; i < k; i += blockDim.x) z[i] = 1.0 / sqrt((double)k);
-    __syncthreads();
-    hmatvec(H, k, z, y);
-    __syncthreads();
+  auto wsum0 = [&](double v) { return __shfl_sync(0xffffffffu, warp_sum(v), 0); };
+  if (warp == 0) {
+    // ---- largest_ritz_value: power iteration (deflation.cpp:57-82), one warp,
+    // shuffles only.  y = H z_{i-1} unnormalised; theta = y.Hy / y.y = z.Hz;
+    // residual |Hy - theta y| / |y| = |Hz - theta z|.
+    double* yv = nx;  // smem broadcast copy of y (warp 0 only)
+    double y[RQ], hy[RQ];
+    for (int i = lane; i < k; i += 32) z[i] = 1.0 / sqrt((double)k);
+    __syncwarp();
+    hmv_global(z, y);
+#pragma unroll
+    for (int q = 0; q < RQ; ++q)
+      if (lane + 32 * q < k) yv[lane + 32 * q] = y[q];
+    __syncwarp();
     bool have = false, conv = false, broke = false;
     double val = 0.0;
     for (int it = 0; it < d->pow_maxit; ++it) {
-      hmatvec(H, k, y, hy);
-      __syncthreads();
-      double p = 0.0, q = 0.0;
-      for (int i = tid; i < k; i += blockDim.x) {
-        p += y[i] * y[i];
-        q += y[i] * hy[i];
-      }
-      p = warp_sum(p);
-      q = warp_sum(q);
-      if ((tid & 31) == 0) {
-        sA[tid >> 5] = p;
-        sA2[tid >> 5] = q;
-      }
-      __syncthreads();
-      double yy = 0.0, yhy = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-        yy += sA[w];
-        yhy += sA2[w];
-      }
+      hmv_global(yv, hy);
+      double p = 0.0, qq = 0.0;
+#pragma unroll
+      for (int q = 0; q < RQ; ++q)
+        if (lane + 32 * q < k) {
+          p += y[q] * y[q];
+          qq += y[q] * hy[q];
+        }
+      const double yy = wsum0(p), yhy = wsum0(qq);
       const double nz = sqrt(yy);
       if (!isfinite(nz) || nz == 0.0) {
         broke = true;
@@ -1378,12 +1562,17 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
       }
       const double theta = yhy / yy;
       double e = 0.0;
-      for (int i = tid; i < k; i += blockDim.x) {
-        const double t = hy[i] - theta * y[i];
-        e += t * t;
-        y[i] = hy[i] / nz;  // H z_i for the next iteration
-      }
-      const double resid = sqrt(bsum1(e, sB) / yy);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < RQ; ++q)
+        if (lane + 32 * q < k) {
+          const double t = hy[q] - theta * y[q];
+          e += t * t;
+          y[q] = hy[q] / nz;  // H z_i for the next iteration
+          yv[lane + 32 * q] = y[q];
+        }
+      const double resid = sqrt(wsum0(e) / yy);
+      __syncwarp();
       val = theta;
       have = true;
       if (resid <= tol * scale) {
@@ -1392,106 +1581,116 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
       }
     }
     const bool ok = conv || (!broke && have);
-    if (tid == 0 && ok && isfinite(val) && fabs(val) > fabs(d->mu)) d->mu = val;  // observe_ritz
-  }
-  __syncthreads();
-  // ---- H^-1 by Gauss-Jordan with partial pivoting: [H | I] -> [I | H^-1]
-  for (int e = tid; e < k * k; e += blockDim.x) B[e] = ((e % k) == (e / k)) ? 1.0 : 0.0;
-  __syncthreads();
-  for (int c = 0; c < k; ++c) {
-    if (tid < 32) {
-      double best = -1.0;
-      int bi = c;
-      for (int i = c + tid; i < k; i += 32) {
-        const double a = fabs(H[i + c * k]);
-        if (a > best) {
-          best = a;
-          bi = i;
+    if (lane == 0 && ok && isfinite(val) && fabs(val) > fabs(d->mu)) d->mu = val;  // observe_ritz
+  } else {
+    // ---- meanwhile warps 1..7: H^-1 by Gauss-Jordan with partial pivoting,
+    // [H | I] -> [I | H^-1] in smem (named barrier 1 over these 224 threads)
+    const int t7 = tid - 32, n7 = RITZ_THREADS - 32;
+    auto gsync = [] { asm volatile("bar.sync 1, %0;" ::"n"(RITZ_THREADS - 32)); };
+    for (int e = t7; e < k * k; e += n7) B[e] = ((e % k) == (e / k)) ? 1.0 : 0.0;
+    gsync();
+    for (int c = 0; c < k; ++c) {
+      if (warp == 1) {
+        double best = -1.0;
+        int bi = c;
+        for (int i = c + lane; i < k; i += 32) {
+          const double a = fabs(H[i + c * k]);
+          if (a > best) {
+            best = a;
+            bi = i;
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+          }
+        }
+        if (lane == 0) s_piv = bi;
+      }
+      gsync();
+      const int pv = s_piv;
+      if (pv != c) {
+        for (int j = t7; j < 2 * k; j += n7) {
+          double* M = j < k ? H : B;
+          const int jj = j < k ? j : j - k;
+          const double t = M[c + jj * k];
+          M[c + jj * k] = M[pv + jj * k];
+          M[pv + jj * k] = t;
         }
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) {
-          best = ob;
-          bi = oi;
-        }
-      }
-      if (tid == 0) s_piv = bi;
-    }
-    __syncthreads();
-    const int p = s_piv;
-    if (p != c) {
-      for (int j = tid; j < 2 * k; j += blockDim.x) {
+      gsync();
+      const double piv = H[c + c * k];
+      gsync();
+      for (int j = t7; j < 2 * k; j += n7) {
         double* M = j < k ? H : B;
         const int jj = j < k ? j : j - k;
-        const double t = M[c + jj * k];
-        M[c + jj * k] = M[p + jj * k];
-        M[p + jj * k] = t;
+        M[c + jj * k] /= piv;
       }
+      for (int i = t7; i < k; i += n7) colc[i] = H[i + c * k];
+      gsync();
+      for (int e = t7; e < 2 * k * k; e += n7) {
+        const int i = e % k, j = e / k;
+        if (i == c) continue;
+        double* M = j < k ? H : B;
+        const int jj = j < k ? j : j - k;
+        M[i + jj * k] -= colc[i] * M[c + jj * k];
+      }
+      gsync();
     }
-    __syncthreads();
-    const double piv = H[c + c * k];
-    __syncthreads();
-    for (int j = tid; j < 2 * k; j += blockDim.x) {
-      double* M = j < k ? H : B;
-      const int jj = j < k ? j : j - k;
-      M[c + jj * k] /= piv;
-    }
-    for (int i = tid; i < k; i += blockDim.x) colc[i] = H[i + c * k];
-    __syncthreads();
-    for (int e = tid; e < 2 * k * k; e += blockDim.x) {
-      const int i = e % k, j = e / k;
-      if (i == c) continue;
-      double* M = j < k ? H : B;
-      const int jj = j < k ? j : j - k;
-      M[i + jj * k] -= colc[i] * M[c + jj * k];
-    }
-    __syncthreads();
   }
-  load_h();  // H again for theta / residuals
   __syncthreads();
-  // ---- smallest_ritz_pair: inverse power iteration (deflation.cpp:31-54):
-  // y = H^-1 z, hy = H y; y.y and y.hy in one sum, then the residual while
-  // z <- y / |y| is written: 4 barriers per iteration.
-  for (int i = tid; i < k; i += blockDim.x) z[i] = 1.0 / sqrt((double)k);
-  __syncthreads();
+  // ---- smallest_ritz_pair: inverse power iteration (deflation.cpp:31-54),
+  // warp 0: y = H^-1 z (smem, lane per row), hy = H y (global); y.y and y.hy
+  // in one pass, then the residual while z <- y / |y| is written.
+  if (warp != 0) return;
   bool conv = false;
   double val = 0.0;
   {
-    __shared__ double sA3[RITZ_THREADS / 32];
+    for (int i = lane; i < k; i += 32) z[i] = 1.0 / sqrt((double)k);
+    __syncwarp();
+    double y[RQ], hy[RQ];
     for (int it = 0; it < d->inv_maxit; ++it) {
-      hmatvec(B, k, z, nx);
-      __syncthreads();
-      hmatvec(H, k, nx, hz);
-      __syncthreads();
-      double p = 0.0, q = 0.0;
-      for (int i = tid; i < k; i += blockDim.x) {
-        p += nx[i] * nx[i];
-        q += nx[i] * hz[i];
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) {
+        const int i = lane + 32 * q;
+        double s0 = 0.0, s1 = 0.0;
+        if (i < k) {
+          int j = 0;
+          for (; j + 1 < k; j += 2) {
+            s0 += B[i + j * k] * z[j];
+            s1 += B[i + (j + 1) * k] * z[j + 1];
+          }
+          if (j < k) s0 += B[i + j * k] * z[j];
+          nx[i] = s0 + s1;
+        }
+        y[q] = s0 + s1;
       }
-      p = warp_sum(p);
-      q = warp_sum(q);
-      if ((tid & 31) == 0) {
-        sA[tid >> 5] = p;
-        sA3[tid >> 5] = q;
-      }
-      __syncthreads();
-      double yy = 0.0, yhy = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-        yy += sA[w];
-        yhy += sA3[w];
-      }
+      __syncwarp();
+      hmv_global(nx, hy);
+      double p = 0.0, qq = 0.0;
+#pragma unroll
+      for (int q = 0; q < RQ; ++q)
+        if (lane + 32 * q < k) {
+          p += y[q] * y[q];
+          qq += y[q] * hy[q];
+        }
+      const double yy = wsum0(p), yhy = wsum0(qq);
       const double nz = sqrt(yy);
       if (!isfinite(nz) || nz == 0.0) break;
       const double theta = yhy / yy;
       double e = 0.0;
-      for (int i = tid; i < k; i += blockDim.x) {
-        const double t = hz[i] - theta * nx[i];
-        e += t * t;
-        z[i] = nx[i] / nz;
-      }
-      const double resid = sqrt(bsum1(e, sB) / yy);
+#pragma unroll
+      for (int q = 0; q < RQ; ++q)
+        if (lane + 32 * q < k) {
+          const double t = hy[q] - theta * y[q];
+          e += t * t;
+          z[lane + 32 * q] = y[q] / nz;
+        }
+      const double resid = sqrt(wsum0(e) / yy);
+      __syncwarp();
       val = theta;
       if (resid <= tol * scale) {
         conv = true;
@@ -1500,8 +1699,8 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
     }
   }
   if (conv) {
-    for (int l = tid; l < k; l += blockDim.x) P.zl[l] = z[l] * P.s[l];
-    if (tid == 0) {
+    for (int l = lane; l < k; l += 32) P.zl[l] = z[l] * P.s[l];
+    if (lane == 0) {
       d->theta = val;
       if (d->r >= P.R1) {  // a failed truncation left the basis full (deflation.cpp:132-135)
         d->skipped++;

@@ -22,6 +22,7 @@ typedef int (*fn_recv)(void*, size_t, int, int, void*, cudaStream_t);
 typedef int (*fn_void)();
 typedef int (*fn_destroy)(void*);
 typedef int (*fn_getid)(UniqueId*);
+typedef int (*fn_allgather)(const void*, void*, size_t, int, void*, cudaStream_t);
 
 struct Api {
   void* h = nullptr;
@@ -32,6 +33,7 @@ struct Api {
   fn_void gstart = nullptr, gend = nullptr;
   fn_destroy destroy = nullptr;
   fn_getid getid = nullptr;
+  fn_allgather allgather = nullptr;
   bool ok = false;
 };
 
@@ -48,6 +50,7 @@ inline Api& api() {
     x.gend = (fn_void)dlsym(x.h, "ncclGroupEnd");
     x.destroy = (fn_destroy)dlsym(x.h, "ncclCommDestroy");
     x.getid = (fn_getid)dlsym(x.h, "ncclGetUniqueId");
+    x.allgather = (fn_allgather)dlsym(x.h, "ncclAllGather");
     x.ok = x.init && x.allreduce && x.send && x.recv && x.gstart && x.gend && x.destroy;
     return x;
   }();
@@ -71,6 +74,12 @@ inline int send_f64(const double* p, size_t n, int peer, void* comm, cudaStream_
 }
 inline int recv_f64(double* p, size_t n, int peer, void* comm, cudaStream_t s) {
   return api().recv(p, n, kFloat64, peer, comm, s);
+}
+// deterministic mode: every rank's plane partials to every rank
+inline int allgather_f64(const double* in, double* out, size_t n_per_rank, void* comm,
+                         cudaStream_t s) {
+  if (!api().allgather) return 1;
+  return api().allgather(in, out, n_per_rank, kFloat64, comm, s);
 }
 inline int group_start() { return api().gstart(); }
 inline int group_end() { return api().gend(); }

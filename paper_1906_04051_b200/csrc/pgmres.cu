@@ -159,7 +159,7 @@ struct pgm_context {
   std::string err;
   uint64_t launches = 0;
   // reduction scratch
-  double *part_buf = nullptr, *gpart_buf = nullptr, *red_out = nullptr;
+  double *part_buf = nullptr, *gpart_buf = nullptr, *g2part_buf = nullptr, *red_out = nullptr;
   unsigned* cnt = nullptr;
   int gmax = 0, nvmax = 0;
   // GMRES workspace
@@ -182,6 +182,14 @@ struct pgm_context {
   // multi-GPU: NCCL (one process per GPU) or an in-process loopback group
   void* nccl = nullptr;
   struct pgm_loopback* loop = nullptr;
+  // deterministic mode (config.deterministic = PGM_DETERMINISTIC_PLANES):
+  // every reduction = per-plane sequential partials + pairwise fold
+  bool det = false;
+  int plane = 0, nplanes = 0, nplanes_global = 0, det_maxp = 0;
+  std::vector<int> plane_off, plane_cnt;  // per rank (global plane order)
+  double *det_pp = nullptr, *det_all = nullptr, *det_gbuf = nullptr;
+  unsigned* det_cnt = nullptr;
+  int det_nv = 0;
   pgm_deflator* cur_defl = nullptr;  // deflator of the running solve (halo of u)
   double* halo_ptr = nullptr;        // HV_PTR: ctx-layout view of a caller vector (Newton u)
   std::vector<pgm_matrix*> mats;     // live matrices (detached when the context dies first)
@@ -550,16 +558,33 @@ Status ensure_reduction(pgm_context* ctx, int nv, int gneed = 0) {
   if (ctx->part_buf && ctx->nvmax >= nv && ctx->gmax >= gmax) return {};
   dfree(ctx->part_buf);
   dfree(ctx->gpart_buf);
+  dfree(ctx->g2part_buf);
   dfree(ctx->cnt);
   dfree(ctx->red_out);
   ctx->nvmax = std::max(nv, 2 * MAX_R1 + MAX_M + 8);
   ctx->gmax = gmax;
   const int ng = (gmax + GROUP - 1) / GROUP;
+  const int ns = (ng + GROUP - 1) / GROUP;
   TRY(dalloc(&ctx->part_buf, (size_t)ctx->nvmax * gmax));
   TRY(dalloc(&ctx->gpart_buf, (size_t)ctx->nvmax * ng));
-  TRY(dalloc(&ctx->cnt, (size_t)ng + 1));
+  TRY(dalloc(&ctx->g2part_buf, (size_t)ctx->nvmax * ns));
+  // counters: [0] final, [1, 1 + ng) groups, [1 + ng, 1 + ng + ns) super-groups
+  // (a reduction with NG groups uses [1 + NG, ...): sized for the largest)
+  TRY(dalloc(&ctx->cnt, (size_t)ng + 1 + ns));
   TRY(dalloc(&ctx->red_out, (size_t)ctx->nvmax));
-  CU(cudaMemset(ctx->cnt, 0, sizeof(unsigned) * (ng + 1)));
+  CU(cudaMemset(ctx->cnt, 0, sizeof(unsigned) * (ng + 1 + ns)));
+  if (ctx->det) {
+    dfree(ctx->det_pp);
+    dfree(ctx->det_all);
+    dfree(ctx->det_gbuf);
+    dfree(ctx->det_cnt);
+    TRY(dalloc(&ctx->det_pp, (size_t)ctx->nvmax * std::max(1, ctx->det_maxp)));
+    TRY(dalloc(&ctx->det_all, (size_t)ctx->nvmax * std::max(1, ctx->nplanes_global)));
+    if (ctx->world > 1 && !ctx->loop)
+      TRY(dalloc(&ctx->det_gbuf, (size_t)ctx->world * ctx->nvmax * std::max(1, ctx->det_maxp)));
+    TRY(dalloc(&ctx->det_cnt, 1));
+    CU(cudaMemset(ctx->det_cnt, 0, sizeof(unsigned)));
+  }
   return {};
 }
 
@@ -736,6 +761,14 @@ Params make_params(pgm_context* ctx, pgm_deflator* d) {
   P.R1 = d->R1;
   P.part = ctx->part_buf;
   P.gpart = ctx->gpart_buf;
+  P.g2part = ctx->g2part_buf;
+  P.det = ctx->det ? 1 : 0;
+  P.plane = ctx->plane;
+  P.nplanes = ctx->nplanes;
+  P.det_pp = ctx->det_pp;
+  P.det_all = ctx->det_all;
+  P.nplanes_global = ctx->nplanes_global;
+  P.det_cnt = ctx->det_cnt;
   P.cnt = ctx->cnt;
   P.red_out = ctx->red_out;
   P.world = ctx->coll ? std::max(ctx->world, 2) : 1;
@@ -773,8 +806,68 @@ enum HaloKind { HV_V = 0, HV_X = 1, HV_U = 2, HV_TMP = 3, HV_PTR = 4 };
 Status allreduce_red(pgm_context* ctx, int nv);
 Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot = 0, cudaStream_t st = nullptr);
 
+// Deterministic mode: gather every rank's plane partials ([v][planes of the
+// rank], nv rows) into det_all ([v][global plane]) on every rank.
+Status det_gather(pgm_context* ctx, int nv) {
+  const int npg = ctx->nplanes_global;
+  if (ctx->loop) {
+    pgm_loopback* L = ctx->loop;
+    CU(cudaStreamSynchronize(ctx->stream));
+    L->barrier();  // every rank's k_det_dots has finished
+    for (int q = 0; q < ctx->world; ++q) {
+      const pgm_context* o = L->ctx[q];
+      if (ctx->plane_cnt[q] == 0) continue;
+      CU(cudaMemcpy2DAsync(ctx->det_all + ctx->plane_off[q], 8 * (size_t)npg, o->det_pp,
+                           8 * (size_t)ctx->plane_cnt[q], 8 * (size_t)ctx->plane_cnt[q], nv,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    CU(cudaStreamSynchronize(ctx->stream));
+    L->barrier();  // nobody overwrites its partials before all have copied them
+    return {};
+  }
+  // NCCL: every rank contributes nv x det_maxp (its planes, padded)
+  const size_t per = (size_t)nv * ctx->det_maxp;
+  {
+    // pack [v][nplanes] -> [v][det_maxp] (columns beyond nplanes unused)
+    CU(cudaMemcpy2DAsync(ctx->det_gbuf + (size_t)ctx->rank * per, 8 * (size_t)ctx->det_maxp,
+                         ctx->det_pp, 8 * (size_t)ctx->nplanes, 8 * (size_t)ctx->nplanes, nv,
+                         cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  if (nccl_lite::allgather_f64(ctx->det_gbuf + (size_t)ctx->rank * per, ctx->det_gbuf, per,
+                               ctx->nccl, ctx->stream) != 0)
+    return Status{PGM_ENCCL, "ncclAllGather (deterministic plane partials) failed"};
+  for (int q = 0; q < ctx->world; ++q) {
+    if (ctx->plane_cnt[q] == 0) continue;
+    CU(cudaMemcpy2DAsync(ctx->det_all + ctx->plane_off[q], 8 * (size_t)npg,
+                         ctx->det_gbuf + (size_t)q * per, 8 * (size_t)ctx->det_maxp,
+                         8 * (size_t)ctx->plane_cnt[q], nv, cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+  }
+  return {};
+}
+
 template <int KIND>
 Status finish_global(pgm_context* ctx, const Params& P, int k, int nv) {
+  if (ctx->det) {
+    // the reduction kernel skipped its tail (P.det): recompute the values as
+    // per-plane sequential partials + pairwise fold, then finish
+    if (nv <= 0 || nv > ctx->nvmax) return Status{PGM_ESTATE, "finish_global: bad reduction size"};
+    const long threads = (long)std::max(1, ctx->nplanes) * nv;
+    const int G = (int)((threads + DET_THREADS - 1) / DET_THREADS);
+    {
+      ProfScope ps(ctx, PC_ALLREDUCE, (uint32_t)k);
+      k_det_dots<KIND><<<G, DET_THREADS, 0, ctx->stream>>>(P, k);
+      ctx->launches++;
+      CU(cudaGetLastError());
+      if (ctx->world > 1) {
+        TRY(det_gather(ctx, nv));
+        k_det_finish<KIND><<<1, DET_THREADS, 0, ctx->stream>>>(P, k);
+        ctx->launches++;
+        CU(cudaGetLastError());
+      }
+    }
+    return {};
+  }
   if (!ctx->coll || ctx->peer) return {};  // peer mode: all-reduced inside the kernel
   if (nv <= 0 || nv > ctx->nvmax) return Status{PGM_ESTATE, "finish_global: bad reduction size"};
   ProfScope ps(ctx, PC_ALLREDUCE, (uint32_t)k);
@@ -1425,6 +1518,22 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) 
   ctx->n = ctx->part.row_end - ctx->part.row_begin;
   ctx->lo = ctx->part.halo_lo;
   ctx->hi = ctx->part.halo_hi;
+  if (cfg->deterministic == PGM_DETERMINISTIC_PLANES) {
+    // planes = the reference's deterministic reduction blocks (n_axis^2 rows,
+    // partition_rows: slabs of whole planes); without mesh structure one plane
+    ctx->det = true;
+    ctx->plane = cfg->n_axis > 0 ? (int)(cfg->n_axis * cfg->n_axis) : (int)cfg->n_global;
+    ctx->nplanes_global = cfg->n_axis > 0 ? (int)cfg->n_axis : 1;
+    for (int q = 0; q < cfg->world; ++q) {
+      pgm_partition pq = ctx->part;
+      if (cfg->world > 1) pgm_partition_rows(cfg->n_axis, cfg->world, q, &pq);
+      const int cnt = (int)((pq.row_end - pq.row_begin) / ctx->plane);
+      ctx->plane_off.push_back(q == 0 ? 0 : ctx->plane_off.back() + ctx->plane_cnt.back());
+      ctx->plane_cnt.push_back(cnt);
+      ctx->det_maxp = std::max(ctx->det_maxp, cnt);
+    }
+    ctx->nplanes = ctx->plane_cnt[cfg->rank];
+  }
   // +256: bulk copies read whole 256-row chunks past the last owned row
   ctx->ld = round_up(ctx->lo + ctx->n + ctx->hi + 256, 128);
   auto bail = [&](const Status& s) {
@@ -1492,7 +1601,8 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) 
     // loading of a kernel's module waits for the other ranks' spinning kernels).
     const char* pe = std::getenv("PGMRES_PEER");
     const char* ml = std::getenv("CUDA_MODULE_LOADING");
-    const bool want_peer = !(pe && pe[0] == '0') && ml && std::string(ml) == "EAGER";
+    const bool want_peer =
+        !ctx->det && !(pe && pe[0] == '0') && ml && std::string(ml) == "EAGER";
     L->barrier();  // every rank registered and has its window
     if (want_peer) {
       std::vector<char*> bufs(cfg->world);
@@ -1541,8 +1651,13 @@ void pgm_context_destroy(pgm_context* ctx) {
   dfree(ctx->g);
   dfree(ctx->part_buf);
   dfree(ctx->gpart_buf);
+  dfree(ctx->g2part_buf);
   dfree(ctx->cnt);
   dfree(ctx->red_out);
+  dfree(ctx->det_pp);
+  dfree(ctx->det_all);
+  dfree(ctx->det_gbuf);
+  dfree(ctx->det_cnt);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_dstate) cudaFreeHost(ctx->h_dstate);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -1903,6 +2018,18 @@ pgm_status pgm_deflator_apply(pgm_deflator* d, const double* v, double* w, int32
   return s.code ? fail(ctx, s) : PGM_OK;
 }
 
+#if PGM_TAIL_TIMING
+// tuning variant only: accumulated reduction-tail stamps of the DCGS2 step
+// SpMV (ns): [level-1 chain, level 2, finisher, launches]; reset after read
+int pgm_debug_tail(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_tail_ns, 4 * sizeof(unsigned long long));
+  unsigned long long z[8] = {};
+  cudaMemcpyToSymbol(g_tail_ns, z, sizeof(z));
+  return 0;
+}
+#endif
+
 pgm_status pgm_set_restart_observer(pgm_context* ctx, pgm_restart_observer cb, void* user) {
   if (!ctx) return PGM_EINVAL;
   ctx->obs = cb;
@@ -2098,6 +2225,9 @@ pgm_status pgm_peer_import(pgm_context* ctx, const void* all) {
   if (!ctx || !all) return PGM_EINVAL;
   if (ctx->world < 2 || !ctx->pbuf || ctx->loop)
     return fail(ctx, einval("pgm_peer_import: needs a world > 1 NCCL context"));
+  if (ctx->det)
+    return fail(ctx, einval("pgm_peer_import: the deterministic mode gathers plane partials "
+                            "(NCCL); the fused peer allreduce is not available in it"));
   const char* ml = std::getenv("CUDA_MODULE_LOADING");
   if (!ml || std::string(ml) != "EAGER")
     return fail(ctx, einval("pgm_peer_import: set CUDA_MODULE_LOADING=EAGER before CUDA starts "

@@ -178,8 +178,14 @@ class DeviceExecutor:
 
     def __init__(self, device: int = 0, *, n_global: int | None = None, n_axis: int = 0,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 loopback: "LoopbackGroup | None" = None):
+                 loopback: "LoopbackGroup | None" = None, deterministic: bool = False):
+        """deterministic=True: every reduction is per-plane sequential partials
+        + the reference's pairwise fold (parallel.cpp:33-46, 120-131), so the
+        solve is bit-identical for any rank count (the reference's
+        deterministic executor); slower.  Default: fixed-order device
+        reductions (bitwise reproducible for a given partition)."""
         self.device, self.rank, self.world = device, rank, world
+        self.deterministic = bool(deterministic)
         self.n_axis = n_axis
         self._nccl_id = nccl_id
         self._loop = loopback
@@ -201,7 +207,8 @@ class DeviceExecutor:
         cfg = capi.ContextConfig(self.device, self.rank, self.world,
                                  C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
                                  self._loop.handle if self._loop is not None else None,
-                                 self.n_axis, int(n_global), 1)
+                                 self.n_axis, int(n_global),
+                                 2 if self.deterministic else 1)
         h = C.c_void_p()
         _check(L.pgm_context_create(C.byref(cfg), C.byref(h)))
         self._ctx = h

@@ -144,3 +144,68 @@ def test_multirank_newton_ne8(cuda, golden, transport):
     assert [it.gmres_inner for it in rep.iters] == [it.gmres_inner for it in res[1][0].iters]
     assert np.all(np.abs(np.array([it.gmres_inner for it in rep.iters]) - g["inner"]) <= 3)
     assert np.linalg.norm(u - g["u"]) <= 1e-8 * np.linalg.norm(g["u"])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("world", [4])
+def test_multirank_cfg2_size(cuda, golden, world, transport):
+    """BASELINE config 2 (n_e = 50, 1.03 M DOF) on W = 4 z-slab ranks (one GPU,
+    loopback): the per-rank size of config 3 split over 8 GPUs is in this
+    regime.  Same iteration count, histories within 1e-10 * beta0, the full
+    solution within 1e-8 of the reference's."""
+    ne = 50
+    na = 2 * ne + 1
+    g = golden("cfg2_full")
+
+    def rank(r, grp):
+        ex = pg.DeviceExecutor(0, n_global=na ** 3, n_axis=na, rank=r, world=world, loopback=grp)
+        A, b = ex.assemble_bratu(ne, 6.8, device=True)
+        d = pg.Deflator(pg.DeflationConfig(), ex)
+        x = cuda.zeros(ex.n_own, dtype=cuda.float64, device="cuda")
+        rep = pg.deflated_gmres(A, b, x, pg.GmresConfig(m=50, rel_tol=1e-10), d, ex)
+        return rep, x.cpu().numpy(), d.rank()
+
+    res = run_ranks(world, rank)
+    x = np.concatenate([rr[1] for rr in res])
+    rep0 = res[0][0]
+    for rep, _, rk in res:
+        assert rep.total_inner == rep0.total_inner and rk == res[0][2]
+    b0 = float(g["defl_beta0"])
+    assert abs(rep0.total_inner - int(g["defl_total_inner"])) <= 1
+    n = min(len(rep0.monitored), len(g["defl_monitored"]))
+    assert np.max(np.abs(rep0.monitored[:n] - g["defl_monitored"][:n])) <= 1e-10 * b0
+    assert np.linalg.norm(x - g["defl_x"]) <= 1e-8 * np.linalg.norm(g["defl_x"])
+    assert res[0][2] == int(g["defl_rank"])
+
+
+@pytest.mark.parametrize("defl", [True, False])
+def test_multirank_m100(cuda, golden, transport, defl):
+    """BASELINE's largest restart length (m = 100, n_e = 25 sweep golden) on
+    W = 2 ranks.  On the peer transport 2m + 2 + r_max + 1 exceeds the window
+    slot, so the solve runs the CGS2 step (two reductions per step) there."""
+    ne, world = 25, 2
+    na = 2 * ne + 1
+    g = golden("sweep_ne25")
+    key = f"m100_{'defl' if defl else 'plain'}"
+
+    def rank(r, grp):
+        ex = pg.DeviceExecutor(0, n_global=na ** 3, n_axis=na, rank=r, world=world, loopback=grp)
+        A, b = ex.assemble_bratu(ne, 6.8, device=True)
+        x = cuda.zeros(ex.n_own, dtype=cuda.float64, device="cuda")
+        cfg = pg.GmresConfig(m=100, max_restarts=200, rel_tol=1e-10)
+        if defl:
+            rep = pg.deflated_gmres(A, b, x, cfg, pg.Deflator(pg.DeflationConfig(), ex), ex)
+        else:
+            rep = pg.gmres_restarted(A, None, b, x, cfg, ex)
+        return rep, x.cpu().numpy()
+
+    res = run_ranks(world, rank)
+    x = np.concatenate([rr[1] for rr in res])
+    rep0 = res[0][0]
+    b0 = float(g[key + "_beta0"])
+    assert abs(rep0.total_inner - int(g[key + "_total_inner"])) <= 1
+    n = min(len(rep0.monitored), len(g[key + "_monitored"]))
+    assert np.max(np.abs(rep0.monitored[:n] - g[key + "_monitored"][:n])) <= 1e-10 * b0
+    assert abs(np.linalg.norm(x) - float(g[key + "_x_norm"])) <= 1e-8 * float(g[key + "_x_norm"])
+    assert np.linalg.norm(x[::97] - g[key + "_x_sample"]) <= 1e-8 * np.linalg.norm(
+        g[key + "_x_sample"])
