@@ -323,6 +323,40 @@ def run_gpu(a):
     tot_time = sum(v[1] for v in per.values())
     solve_frac = (tot_bytes / prof_total / 1e9) / peak if prof_total else None
 
+    # ---- standalone SpMV microbenchmark: y = A x with x ~ U(-1, 1)
+    # from std::mt19937(11) as acceptance.cpp:437-443 (bit-identical stream)
+    from paper_1906_04051_b200.rng import acceptance_vectors
+
+    part = ex.partition() if world > 1 else {"row_begin": 0, "row_end": n}
+    xv = acceptance_vectors(n_g if world > 1 else n)[0][part["row_begin"]:part["row_end"]]
+    xs = torch.from_numpy(np.ascontiguousarray(xv)).cuda()
+    ys = torch.empty_like(xs)
+    for _ in range(3):
+        ex.spmv(dA, xs, ys)
+    torch.cuda.synchronize()
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    reps = 20
+    s0.record(ext)
+    for _ in range(reps):
+        ex.spmv(dA, xs, ys)
+    s1.record(ext)
+    torch.cuda.synchronize()
+    t_sp = s0.elapsed_time(s1) / 1e3 / reps
+    if dist:
+        tt = torch.tensor([t_sp], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_sp = float(tt.item())
+    b_sp = 12 * nnz_local + 4 * (n + 1) + 16 * n
+    spmv_micro = {"kernel": "k_spmv<PlainEpi> via pgm_spmv", "x": "U(-1,1), std::mt19937(11) "
+                  "stream of acceptance.cpp:437-443", "launches": reps,
+                  "us_per_launch": round(1e6 * t_sp, 2),
+                  "GBps": round(b_sp / t_sp / 1e9, 1), "frac": round(b_sp / t_sp / 1e9 / peak, 4),
+                  "bytes_per_launch": int(b_sp),
+                  "note": "SURVEY 8(d) B_spmv = 12 nnz + 4(n+1) + 16n; the kernel stores "
+                          "16-bit column deltas when gaps fit (10 B / nnz)"}
+    del xs, ys
+
     # ---- e2e through the public API with host buffers --------------------------
     e2e = None
     if not a.no_e2e:
@@ -420,6 +454,7 @@ def run_gpu(a):
                            "note": "all hot-path kernels of one profiled solve, algorithmic "
                                    "bytes / summed kernel time"},
         "spmv_GBps": round(achieved, 1),
+        "spmv_micro": spmv_micro,
         "kernels": kernels,
         "clocks": clk,
         "e2e": e2e,

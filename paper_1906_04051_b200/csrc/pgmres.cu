@@ -12,6 +12,7 @@
 #include <cmath>
 #include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -184,6 +185,11 @@ struct pgm_context {
   struct pgm_loopback* loop = nullptr;
   // deterministic mode (config.deterministic = PGM_DETERMINISTIC_PLANES):
   // every reduction = per-plane sequential partials + pairwise fold
+  cudaStream_t cstream = nullptr;  // host -> device staging copies (matrix upload)
+  void* hpin[2] = {nullptr, nullptr};  // pinned ring for pageable matrix sources
+  size_t hpin_bytes = 0;
+  cudaEvent_t ev_hdma[2] = {nullptr, nullptr};
+  cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_gath[2] = {nullptr, nullptr};
   bool det = false;
   int plane = 0, nplanes = 0, nplanes_global = 0, det_maxp = 0;
   std::vector<int> plane_off, plane_cnt;  // per rank (global plane order)
@@ -1206,31 +1212,100 @@ Status gather_values(pgm_context* ctx, pgm_matrix* M, const uint32_t* rp_src,
     }
     M->chunk_cap = cap;
   }
-  double* sv = nullptr;
-  unsigned* sc = nullptr;
-  const size_t cap = std::max<unsigned long long>(M->chunk_cap, 1);
-  TRY(dalloc_async(&sv, cap, st));
-  Status s;
-  if (write_cols) s = dalloc_async(&sc, cap, st);
-  cudaError_t e = cudaSuccess;
-  for (const auto& c : M->chunks) {
-    if (s.code || e != cudaSuccess) break;
-    const size_t cnt = c.hi - c.lo;
-    // stream order makes reuse of the one staging buffer safe: the next
-    // copy starts after the previous chunk's gather
-    e = cudaMemcpyAsync(sv, v_src + c.lo, 8 * cnt, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess && write_cols)
-      e = cudaMemcpyAsync(sc, ci_src + c.lo, 4 * cnt, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) {
-      const size_t blocks = ((size_t)c.count * 32 + threads - 1) / threads;
-      k_csr_to_sell<<<(unsigned)blocks, threads, 0, st>>>(M->view(), M->val, M->col, M->rp, sc,
-                                                          sv, M->col_shift, c.s0, c.count, c.lo,
-                                                          write_cols ? 1 : 0);
-      e = cudaGetLastError();
+  // two staging buffers: the copy of chunk i+1 (copy stream) overlaps the
+  // gather of chunk i (library stream); events order buffer reuse
+  if (!ctx->cstream) {
+    CU(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CU(cudaEventCreateWithFlags(&ctx->ev_copy[b], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&ctx->ev_gath[b], cudaEventDisableTiming));
     }
   }
-  dfree_async(sv, st);
-  dfree_async(sc, st);
+  double* sv[2] = {nullptr, nullptr};
+  unsigned* sc[2] = {nullptr, nullptr};
+  const size_t cap = std::max<unsigned long long>(M->chunk_cap, 1);
+  const int nbuf = M->chunks.size() > 1 ? 2 : 1;
+  Status s;
+  for (int b = 0; b < nbuf && !s.code; ++b) {
+    s = dalloc_async(&sv[b], cap, st);
+    if (!s.code && write_cols) s = dalloc_async(&sc[b], cap, st);
+  }
+  cudaError_t e = cudaSuccess;
+  if (!s.code) e = cudaEventRecord(ctx->ev_gath[0], st);  // buffers allocated (stream order)
+  if (e == cudaSuccess && nbuf > 1) e = cudaEventRecord(ctx->ev_gath[1], st);
+  // pageable sources (a std::vector, a numpy array): the driver would stage
+  // them through its own pinned buffer with one host thread (~13 GB/s); here
+  // host threads copy chunk i into a pinned ring while the DMA moves chunk
+  // i - 1 (PCIe rate)
+  cudaPointerAttributes pa{};
+  const bool pageable = cudaPointerGetAttributes(&pa, v_src) != cudaSuccess ||
+                        pa.type == cudaMemoryTypeUnregistered;
+  cudaGetLastError();
+  const size_t pin_bytes = cap * (write_cols ? 12 : 8);
+  if (pageable && ctx->hpin_bytes < pin_bytes) {
+    for (int b = 0; b < 2; ++b) {
+      if (ctx->hpin[b]) cudaFreeHost(ctx->hpin[b]);
+      ctx->hpin[b] = nullptr;
+      if (!ctx->ev_hdma[b]) CU(cudaEventCreateWithFlags(&ctx->ev_hdma[b], cudaEventDisableTiming));
+    }
+    ctx->hpin_bytes = 0;
+    if (cudaHostAlloc(&ctx->hpin[0], pin_bytes, cudaHostAllocDefault) == cudaSuccess &&
+        cudaHostAlloc(&ctx->hpin[1], pin_bytes, cudaHostAllocDefault) == cudaSuccess) {
+      ctx->hpin_bytes = pin_bytes;
+    } else {  // no pinned memory: the driver's own staging
+      cudaGetLastError();
+      for (int b = 0; b < 2; ++b)
+        if (ctx->hpin[b]) cudaFreeHost(ctx->hpin[b]), ctx->hpin[b] = nullptr;
+    }
+  }
+  const bool ring = pageable && ctx->hpin_bytes >= pin_bytes;
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  auto par_copy = [hw](char* dst, const char* src, size_t bytes) {
+    const size_t per = (bytes + hw - 1) / hw;
+    std::vector<std::thread> team;
+    for (unsigned t = 1; t < hw && t * per < bytes; ++t)
+      team.emplace_back([=] { std::memcpy(dst + t * per, src + t * per, std::min(per, bytes - t * per)); });
+    std::memcpy(dst, src, std::min(per, bytes));
+    for (auto& th : team) th.join();
+  };
+  for (size_t i = 0; i < M->chunks.size(); ++i) {
+    if (s.code || e != cudaSuccess) break;
+    const auto& c = M->chunks[i];
+    const int b = (int)(i % nbuf);
+    const size_t cnt = c.hi - c.lo;
+    const double* vsrc = v_src + c.lo;
+    const uint32_t* csrc = write_cols ? ci_src + c.lo : nullptr;
+    if (ring) {
+      // the DMA that last read pinned buffer b must be done before refilling it
+      const int hb = (int)(i % 2);
+      if (i >= 2) e = cudaEventSynchronize(ctx->ev_hdma[hb]);
+      char* hp = static_cast<char*>(ctx->hpin[hb]);
+      par_copy(hp, reinterpret_cast<const char*>(vsrc), 8 * cnt);
+      if (write_cols) par_copy(hp + 8 * cnt, reinterpret_cast<const char*>(csrc), 4 * cnt);
+      vsrc = reinterpret_cast<const double*>(hp);
+      if (write_cols) csrc = reinterpret_cast<const uint32_t*>(hp + 8 * cnt);
+    }
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->cstream, ctx->ev_gath[b], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(sv[b], vsrc, 8 * cnt, cudaMemcpyHostToDevice, ctx->cstream);
+    if (e == cudaSuccess && write_cols)
+      e = cudaMemcpyAsync(sc[b], csrc, 4 * cnt, cudaMemcpyHostToDevice, ctx->cstream);
+    if (e == cudaSuccess && ring) e = cudaEventRecord(ctx->ev_hdma[i % 2], ctx->cstream);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_copy[b], ctx->cstream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ctx->ev_copy[b], 0);
+    if (e == cudaSuccess) {
+      const size_t blocks = ((size_t)c.count * 32 + threads - 1) / threads;
+      k_csr_to_sell<<<(unsigned)blocks, threads, 0, st>>>(M->view(), M->val, M->col, M->rp,
+                                                          sc[b], sv[b], M->col_shift, c.s0,
+                                                          c.count, c.lo, write_cols ? 1 : 0);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_gath[b], st);
+  }
+  for (int b = 0; b < 2; ++b) {
+    dfree_async(sv[b], st);
+    dfree_async(sc[b], st);
+  }
   if (s.code) return s;
   CU(e);
   return {};
@@ -1658,6 +1733,15 @@ void pgm_context_destroy(pgm_context* ctx) {
   dfree(ctx->det_all);
   dfree(ctx->det_gbuf);
   dfree(ctx->det_cnt);
+  if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
+  for (int b = 0; b < 2; ++b) {
+    if (ctx->hpin[b]) cudaFreeHost(ctx->hpin[b]);
+    if (ctx->ev_hdma[b]) cudaEventDestroy(ctx->ev_hdma[b]);
+  }
+  for (int b = 0; b < 2; ++b) {
+    if (ctx->ev_copy[b]) cudaEventDestroy(ctx->ev_copy[b]);
+    if (ctx->ev_gath[b]) cudaEventDestroy(ctx->ev_gath[b]);
+  }
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_dstate) cudaFreeHost(ctx->h_dstate);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
