@@ -179,6 +179,23 @@ def _pct(v, parts):
     return 100.0 * v / t if t > 0 else 0.0
 
 
+def speedup_rows(dof, results):
+    """Rows of one mesh from [(p, median_s, (compute_s, local_s, global_s))]
+    with p = 1 first (bratu_bench.cpp:282-307): speedup = T1 / Tp,
+    relative_speed = slowest / Tp, percentages of the summed clocks
+    (TimingBreakdown, parallel.hpp:47-62)."""
+    t1 = next((m for p, m, _ in results if p == 1), 0.0)
+    rows = [{"dof": dof, "p": p, "median_s": med,
+             "speedup": t1 / med if t1 > 0 else 1.0, "relative_speed": 1.0,
+             "compute_pct": _pct(parts[0], parts), "local_comm_pct": _pct(parts[1], parts),
+             "global_comm_pct": _pct(parts[2], parts)} for p, med, parts in results]
+    if rows:
+        slowest = max(r["median_s"] for r in rows)
+        for r in rows:
+            r["relative_speed"] = slowest / r["median_s"]
+    return rows
+
+
 def _timed_solves(ex, dist, dA, b, cfg, rmax, reps):
     """One warm-up + `reps` fixed-iteration deflated solves with a fresh
     Deflator each (bratu_bench.cpp:282-300); the median by device time (max
@@ -262,8 +279,7 @@ def cmd_speedup(a) -> int:
     rows = []
     for ne in a.ne:
         cfg = pg.GmresConfig(m=a.m, max_restarts=a.restarts, fixed_iterations=True)
-        first = len(rows)
-        t1 = 0.0
+        results = []
         for p in ps:
             if p > 1 and a.loopback > 1:
                 res = _loopback_solves(ne, p, a, cfg)
@@ -287,18 +303,8 @@ def cmd_speedup(a) -> int:
                 ex.close()
             if rank != 0:
                 continue
-            med, parts = res
-            if p == 1:
-                t1 = med
-            rows.append({"dof": (2 * ne + 1) ** 3, "p": p, "median_s": med,
-                         "speedup": t1 / med if t1 > 0 else 1.0, "relative_speed": 1.0,
-                         "compute_pct": _pct(parts[0], parts),
-                         "local_comm_pct": _pct(parts[1], parts),
-                         "global_comm_pct": _pct(parts[2], parts)})
-        if rows[first:]:
-            slowest = max(r["median_s"] for r in rows[first:])
-            for r in rows[first:]:
-                r["relative_speed"] = slowest / r["median_s"]
+            results.append((p, res[0], res[1]))
+        rows.extend(speedup_rows((2 * ne + 1) ** 3, results))
     lead = rank == 0
     sink = _Sink(a, "speedup", lead)
     sink.write("dof,p,median_s,speedup,relative_speed,compute_pct,local_comm_pct,"
