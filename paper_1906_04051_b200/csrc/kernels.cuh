@@ -668,6 +668,111 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
 }
 
 // ---------------------------------------------------------------------------
+// x update at the end of a cycle: x += V xc + U cx (gmres.cpp:183-188, with
+// M^{-1} of the correction folded into U cx through the cached U^T V; the
+// coefficients come from k_end_cycle).  Streaming like the DCGS2 update: a
+// warp per 64-row chunk, 2 rows per lane, the basis and U columns read in
+// batches of 4 double2 loads per lane.
+constexpr int XU_BLOCK = 256;
+__global__ void __launch_bounds__(XU_BLOCK) k_xupdate(Params P) {
+  __shared__ double cv[MAX_M + MAX_R1 + 8];
+  const GState* g = P.g;
+  if (g->error != 0) return;
+  const int steps = g->steps, r = P.d->r;
+  const int nvec = steps + r;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int l = threadIdx.x; l < nvec + 4; l += XU_BLOCK)
+    cv[l] = l < steps ? P.xc[l] : (l < nvec ? P.cx[l - steps] : 0.0);
+  __syncthreads();
+  const int n = P.n;
+  const size_t ld = P.ld;
+  const double* V0 = P.V + P.lo;
+  const double* U0 = P.U + P.lo;
+  double* x = P.x + P.lo;
+  const int nch = (n + 63) >> 6;
+  const int W = gridDim.x * (XU_BLOCK / 32);
+  for (int c = blockIdx.x * (XU_BLOCK / 32) + warp; c < nch; c += W) {
+    const int row0 = c * 64 + 2 * lane;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int l0 = 0; l0 < nvec; l0 += 4) {
+      double2 t[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int l = l0 + j;
+        const double* base = l < steps ? V0 + (size_t)l * ld : U0 + (size_t)(l - steps) * ld;
+        t[j] = l < nvec ? __ldg(reinterpret_cast<const double2*>(base + row0))
+                        : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc.x += cv[l0 + j] * t[j].x;
+        acc.y += cv[l0 + j] * t[j].y;
+      }
+    }
+    if (row0 + 1 < n) {
+      double2 xv = *reinterpret_cast<const double2*>(x + row0);
+      xv.x += acc.x;
+      xv.y += acc.y;
+      *reinterpret_cast<double2*>(x + row0) = xv;
+    } else if (row0 < n) {
+      x[row0] += acc.x;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// DCGS2 cycle close (a cycle that ran all m steps): red = [W_l . u_m (l < m),
+// u_m . u_m] completes column m-1 (fin_dcgs2_close).  Same scheme as the step
+// SpMV's epilogue: one 512-row tile per block, u_m's rows staged in smem,
+// warp w streams W_w, W_{w+8}, ... with all 16 loads per lane in flight.
+// (The generic k_sweep<SW_DCLOSE> moved 1.5x the algorithmic bytes at 4.2
+// TB/s: its Q set went through the transposed tile.)
+__global__ void __launch_bounds__(SPMV_THREADS) k_dclose(Params P, int ntiles) {
+  extern __shared__ double sm[];
+  pdl_wait();
+  if (!P.g->active) return;
+  const int m = P.m, nv = m + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x;
+  const int row0 = tile * TILE;
+  const int rows = min(TILE, P.n - row0);
+  const size_t ld = P.ld;
+  double* us = sm;
+  double* bvals = us + TILE;
+  double* red = bvals + nv;
+  const double* um = P.V + (size_t)m * ld + P.lo + row0;
+  for (int i = threadIdx.x; i < TILE; i += SPMV_THREADS) us[i] = i < rows ? um[i] : 0.0;
+  __syncthreads();
+  const double* v0 = P.V + P.lo + row0;
+  for (int q = warp; q < nv; q += SPMV_WARPS) {
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    if (q < m) {
+      const double* v = v0 + (size_t)q * ld + lane;
+      if (rows == TILE) {
+        double t[TILE / 32];
+#pragma unroll
+        for (int i = 0; i < TILE / 32; ++i) t[i] = __ldg(v + 32 * i);
+#pragma unroll
+        for (int i = 0; i < TILE / 32; ++i) a[i & 3] += t[i] * us[lane + 32 * i];
+      } else {
+        for (int i = 0; i < TILE / 32; ++i)
+          if (lane + 32 * i < rows) a[i & 3] += __ldg(v + 32 * i) * us[lane + 32 * i];
+      }
+    } else {
+      for (int i = 0; i < TILE / 32; ++i) {
+        const double u = us[lane + 32 * i];
+        a[i & 3] += u * u;
+      }
+    }
+    const double sum = warp_sum((a[0] + a[1]) + (a[2] + a[3]));
+    if (lane == 0) bvals[q] = sum;
+  }
+  pdl_trigger();
+  __syncthreads();
+  if (reduce_tail(bvals, nv, P, red, ntiles, tile)) fin_dcgs2_close(P, red);
+}
+
+// ---------------------------------------------------------------------------
 // Streaming sweeps over basis blocks.
 enum SweepMode {
   SW_CGS2_B = 0,   // w1 = w - V h1 ; dots V^T w1 (staged)
@@ -1457,7 +1562,7 @@ __device__ __forceinline__ void hmatvec(const double* M, int k, const double* z,
   if (i < k && !half) out[i] = s;
 }
 
-__global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
+__global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
   extern __shared__ double sm[];
   GState* g = P.g;
   DState* d = P.d;
@@ -1484,11 +1589,16 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
   double* hz = nx + k;          // k
   double* colc = hz + k;        // k
   __shared__ int s_piv;
+  // hcopy: a third k*k smem block keeps H for warp 0's matvecs while the
+  // Gauss-Jordan inverse consumes the first one (host: when 3 m^2 fits)
+  double* H2 = colc + k;
   auto load_h = [&]() {
     for (int e = tid; e < k * k; e += blockDim.x) {
       const int i = e % k, j = e / k;
       const int top = min(k - 1, j + 1);
-      H[e] = (i <= top) ? P.h_orig[(size_t)j * (m + 1) + i] : 0.0;
+      const double h = (i <= top) ? P.h_orig[(size_t)j * (m + 1) + i] : 0.0;
+      H[e] = h;
+      if (hcopy) H2[e] = h;
     }
   };
   load_h();
@@ -1513,20 +1623,35 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
   const double* hg = P.h_orig;
   const size_t hld = (size_t)m + 1;
   constexpr int RQ = (MAX_M + 31) / 32;  // rows per lane
+  // y = H v, lane per row (Hessenberg: H(i, j) = 0 for j < i - 1), four
+  // independent accumulators so the loads of consecutive columns overlap
   auto hmv_global = [&](const double* v, double (&out)[RQ]) {
 #pragma unroll
     for (int q = 0; q < RQ; ++q) {
       const int i = lane + 32 * q;
-      double s0 = 0.0, s1 = 0.0;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       if (i < k) {
-        int j = i > 0 ? i - 1 : 0;  // Hessenberg: H(i, j) = 0 for j < i - 1
-        for (; j + 1 < k; j += 2) {
-          s0 += __ldg(hg + (size_t)j * hld + i) * v[j];
-          s1 += __ldg(hg + (size_t)(j + 1) * hld + i) * v[j + 1];
+        int j = i > 0 ? i - 1 : 0;
+        if (hcopy) {
+          const double* hr = H2 + i;
+          for (; j + 4 <= k; j += 4) {
+            a0 += hr[(size_t)j * k] * v[j];
+            a1 += hr[(size_t)(j + 1) * k] * v[j + 1];
+            a2 += hr[(size_t)(j + 2) * k] * v[j + 2];
+            a3 += hr[(size_t)(j + 3) * k] * v[j + 3];
+          }
+          for (; j < k; ++j) a0 += hr[(size_t)j * k] * v[j];
+        } else {
+          for (; j + 4 <= k; j += 4) {
+            a0 += __ldg(hg + (size_t)j * hld + i) * v[j];
+            a1 += __ldg(hg + (size_t)(j + 1) * hld + i) * v[j + 1];
+            a2 += __ldg(hg + (size_t)(j + 2) * hld + i) * v[j + 2];
+            a3 += __ldg(hg + (size_t)(j + 3) * hld + i) * v[j + 3];
+          }
+          for (; j < k; ++j) a0 += __ldg(hg + (size_t)j * hld + i) * v[j];
         }
-        if (j < k) s0 += __ldg(hg + (size_t)j * hld + i) * v[j];
       }
-      out[q] = s0 + s1;
+      out[q] = (a0 + a1) + (a2 + a3);
     }
   };
   auto wsum0 = [&](double v) { return __shfl_sync(0xffffffffu, warp_sum(v), 0); };
@@ -1656,17 +1781,19 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P) {
 #pragma unroll
       for (int q = 0; q < RQ; ++q) {
         const int i = lane + 32 * q;
-        double s0 = 0.0, s1 = 0.0;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         if (i < k) {
           int j = 0;
-          for (; j + 1 < k; j += 2) {
-            s0 += B[i + j * k] * z[j];
-            s1 += B[i + (j + 1) * k] * z[j + 1];
+          for (; j + 4 <= k; j += 4) {
+            a0 += B[i + j * k] * z[j];
+            a1 += B[i + (j + 1) * k] * z[j + 1];
+            a2 += B[i + (j + 2) * k] * z[j + 2];
+            a3 += B[i + (j + 3) * k] * z[j + 3];
           }
-          if (j < k) s0 += B[i + j * k] * z[j];
-          nx[i] = s0 + s1;
+          for (; j < k; ++j) a0 += B[i + j * k] * z[j];
+          nx[i] = (a0 + a1) + (a2 + a3);
         }
-        y[q] = s0 + s1;
+        y[q] = (a0 + a1) + (a2 + a3);
       }
       __syncwarp();
       hmv_global(nx, hy);

@@ -919,7 +919,14 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
       TRY(finish_global<103>(ctx, P, k, std::max(k, 1) + k + 2 + R1));
       TRY(launch_dcgs2_update(ctx, P, k));
     }
-    TRY(launch_sweep<SW_DCLOSE>(ctx, P, m, 0, 0, m + 1, false));
+    {
+      const int nt = (int)((ctx->n + TILE - 1) / TILE);
+      const size_t smem = sizeof(double) * ((size_t)TILE + 2 * (m + 1) + 2);
+      ProfScope ps(ctx, PC_OTHER, (uint32_t)m);
+      CU(launch_pdl(ctx, k_dclose, nt, SPMV_THREADS, smem, P, nt));
+      ctx->launches++;
+      CU(cudaGetLastError());
+    }
     TRY(finish_global<SW_DCLOSE>(ctx, P, m, m + 1));
   }
   for (int k = 0; k < (ctx->dc_now ? 0 : m); ++k) {
@@ -961,14 +968,24 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
     ctx->launches++;
     CU(cudaGetLastError());
   }
-  TRY(launch_sweep<SW_XUPDATE>(ctx, P, 0, m, R1, 0, false));
+  {
+    ProfScope ps(ctx, PC_XUPDATE, 0);
+    const int occ = std::min(MAX_BLOCKS_PER_SM, occupancy(k_xupdate, XU_BLOCK, 0));
+    const int nch = (int)((ctx->n + 63) / 64);
+    const int G = std::max(1, std::min((nch + XU_BLOCK / 32 - 1) / (XU_BLOCK / 32), occ * ctx->nsm));
+    k_xupdate<<<G, XU_BLOCK, 0, ctx->stream>>>(P);
+    ctx->launches++;
+    CU(cudaGetLastError());
+  }
   if (harvest) {
-    const size_t rsmem = sizeof(double) * (2 * (size_t)m * m + 4 * m);
+    // [H | H^-1] + 4 vectors, plus a copy of H for the matvecs when it fits
+    const int hcopy = sizeof(double) * (3 * (size_t)m * m + 4 * m) <= 227 * 1024 ? 1 : 0;
+    const size_t rsmem = sizeof(double) * ((2 + hcopy) * (size_t)m * m + 4 * m);
     if (rsmem > 48 * 1024)
       CU(cudaFuncSetAttribute(k_ritz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
     {
       ProfScope ps(ctx, PC_RITZ, 0);
-      k_ritz<<<1, RITZ_THREADS, rsmem, ctx->stream>>>(P);
+      k_ritz<<<1, RITZ_THREADS, rsmem, ctx->stream>>>(P, hcopy);
     }
     ctx->launches++;
     CU(cudaGetLastError());
