@@ -1864,24 +1864,53 @@ __global__ void __launch_bounds__(256) k_rotate(Params P) {
   }
   if (!d->rotate) return;
   const int r0 = d->r0, r = d->r, R1 = P.R1;
-  __shared__ double q[MAX_R1 * MAX_R1];
-  for (int e = threadIdx.x; e < r0 * r; e += blockDim.x) q[e] = P.Q[(e % r0) + (e / r0) * R1];
+  // q stored l-major with the output index j contiguous (padded to even):
+  // one LDS.128 gives two coefficients; each thread rotates a PAIR of rows
+  // (double2 loads), so every coefficient load feeds four FMAs
+  constexpr int QP = MAX_R1 + 1 + (MAX_R1 + 1) % 2;
+  __shared__ __align__(16) double q[MAX_R1 * QP];
+  for (int e = threadIdx.x; e < r0 * QP; e += blockDim.x) {
+    const int l = e / QP, j = e % QP;
+    q[e] = (j < r) ? P.Q[l + (size_t)j * R1] : 0.0;
+  }
   __syncthreads();
-  for (size_t row = blockIdx.x * (size_t)blockDim.x + threadIdx.x; row < (size_t)P.n;
-       row += (size_t)gridDim.x * blockDim.x) {
+  const size_t npair = ((size_t)P.n + 1) / 2;
+  for (size_t pr = blockIdx.x * (size_t)blockDim.x + threadIdx.x; pr < npair;
+       pr += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = 2 * pr;
+    const bool pair = row + 1 < (size_t)P.n;
 #pragma unroll 1
     for (int which = 0; which < 2; ++which) {
       double* base = (which == 0 ? P.U : P.AU) + P.lo + row;
-      double in[MAX_R1];
+      double2 in[MAX_R1];
 #pragma unroll
       for (int l = 0; l < MAX_R1; ++l)
-        if (l < r0) in[l] = base[(size_t)l * P.ld];
-      for (int j = 0; j < r; ++j) {
-        double s = 0.0;
+        if (l < r0) {
+          const double* src = base + (size_t)l * P.ld;
+          in[l] = pair ? *reinterpret_cast<const double2*>(src) : make_double2(src[0], 0.0);
+        }
+      // output columns j, j+1 at a time: one LDS.128 of coefficients feeds
+      // four FMAs (two rows x two outputs); the j loop stays a runtime loop
+      // so the only register array is in[] (compile-time indices)
+      for (int j = 0; j < r; j += 2) {
+        double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
 #pragma unroll
         for (int l = 0; l < MAX_R1; ++l)
-          if (l < r0) s += in[l] * q[l + j * r0];
-        base[(size_t)j * P.ld] = s;
+          if (l < r0) {
+            const double2 qq = *reinterpret_cast<const double2*>(q + l * QP + j);
+            x0 += in[l].x * qq.x;
+            y0 += in[l].y * qq.x;
+            x1 += in[l].x * qq.y;
+            y1 += in[l].y * qq.y;
+          }
+        double* d0 = base + (size_t)j * P.ld;
+        if (pair) *reinterpret_cast<double2*>(d0) = make_double2(x0, y0);
+        else d0[0] = x0;
+        if (j + 1 < r) {
+          double* d1 = d0 + P.ld;
+          if (pair) *reinterpret_cast<double2*>(d1) = make_double2(x1, y1);
+          else d1[0] = x1;
+        }
       }
     }
   }
