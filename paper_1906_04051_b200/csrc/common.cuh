@@ -31,6 +31,9 @@ constexpr int GROUP = 32;             // first-level reduction group (blocks, on
 constexpr int MAX_M = 112;            // Ritz harvest keeps [H | H^-1] in smem
 constexpr int MAX_R1 = 32;            // r_max + 1 bound of the register fast path
 constexpr int RITZ_THREADS = 256;
+#ifndef PGM_RITZ_SEQ
+#define PGM_RITZ_SEQ 0  // tuning: 1 = Gauss-Jordan after (not beside) the power iteration
+#endif
 
 // ---- device state ------------------------------------------------------------
 // Per-solve GMRES control word (gmres.cpp:132-218 loop variables + GmresReport
@@ -169,7 +172,7 @@ constexpr int VPW = PGM_VPW;
 #define PGM_TAIL_TIMING 0  // tuning variant: %globaltimer stamps of the reduction tail
 #endif
 #if PGM_TAIL_TIMING
-__device__ unsigned long long g_tail_ns[8];
+__device__ unsigned long long g_tail_ns[16];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -1617,6 +1617,11 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
   }
   const double tol = d->inv_tol;
   const int warp = tid >> 5, lane = tid & 31;
+#if PGM_TAIL_TIMING
+  const unsigned long long rt0 = gtimer();
+  unsigned long long rt1 = 0;
+  int n_pow = 0, n_inv = 0;
+#endif
   // H (Hessenberg block, column-major i + j (m+1)) read by lane-per-row
   // matvecs straight from P.h_orig (L1-resident after the first sweep): the
   // smem copy is consumed by the Gauss-Jordan inverse that runs meanwhile.
@@ -1634,13 +1639,22 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
         int j = i > 0 ? i - 1 : 0;
         if (hcopy) {
           const double* hr = H2 + i;
-          for (; j + 4 <= k; j += 4) {
-            a0 += hr[(size_t)j * k] * v[j];
-            a1 += hr[(size_t)(j + 1) * k] * v[j + 1];
-            a2 += hr[(size_t)(j + 2) * k] * v[j + 2];
-            a3 += hr[(size_t)(j + 3) * k] * v[j + 3];
+          double a4 = 0.0, a5 = 0.0, a6 = 0.0, a7 = 0.0;
+          for (; j + 8 <= k; j += 8) {
+            a0 += hr[j * k] * v[j];
+            a1 += hr[(j + 1) * k] * v[j + 1];
+            a2 += hr[(j + 2) * k] * v[j + 2];
+            a3 += hr[(j + 3) * k] * v[j + 3];
+            a4 += hr[(j + 4) * k] * v[j + 4];
+            a5 += hr[(j + 5) * k] * v[j + 5];
+            a6 += hr[(j + 6) * k] * v[j + 6];
+            a7 += hr[(j + 7) * k] * v[j + 7];
           }
-          for (; j < k; ++j) a0 += hr[(size_t)j * k] * v[j];
+          for (; j < k; ++j) a0 += hr[j * k] * v[j];
+          a0 += a4;
+          a1 += a5;
+          a2 += a6;
+          a3 += a7;
         } else {
           for (; j + 4 <= k; j += 4) {
             a0 += __ldg(hg + (size_t)j * hld + i) * v[j];
@@ -1655,6 +1669,25 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
     }
   };
   auto wsum0 = [&](double v) { return __shfl_sync(0xffffffffu, warp_sum(v), 0); };
+  // three warp sums with interleaved shuffle chains (lane 0's values broadcast)
+  auto wsum3 = [&](double& a, double& b, double& c) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    a = __shfl_sync(0xffffffffu, a, 0);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    c = __shfl_sync(0xffffffffu, c, 0);
+  };
+  // |Hz - theta z|^2 = |Hy|^2/|y|^2 - theta^2 (Rayleigh quotient theta): from
+  // the same sums, with rounding error <= ~8 eps scale^2.  Far from
+  // convergence this proves resid > tol * scale and the exact residual pass
+  // (a second dependent warp reduction) is skipped; near it, the exact
+  // formula decides, exactly as deflation.cpp:48-52 / 74-78.
+  const double skip_above = fmax(64.0 * 2.220446049250313e-16 * scale * scale,
+                                 4.0 * (tol * scale) * (tol * scale));
   if (warp == 0) {
     // ---- largest_ritz_value: power iteration (deflation.cpp:57-82), one warp,
     // shuffles only.  y = H z_{i-1} unnormalised; theta = y.Hy / y.y = z.Hz;
@@ -1672,20 +1705,23 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
     double val = 0.0;
     for (int it = 0; it < d->pow_maxit; ++it) {
       hmv_global(yv, hy);
-      double p = 0.0, qq = 0.0;
+      double p = 0.0, qq = 0.0, hh = 0.0;
 #pragma unroll
       for (int q = 0; q < RQ; ++q)
         if (lane + 32 * q < k) {
           p += y[q] * y[q];
           qq += y[q] * hy[q];
+          hh += hy[q] * hy[q];
         }
-      const double yy = wsum0(p), yhy = wsum0(qq);
+      wsum3(p, qq, hh);
+      const double yy = p, yhy = qq;
       const double nz = sqrt(yy);
       if (!isfinite(nz) || nz == 0.0) {
         broke = true;
         break;
       }
       const double theta = yhy / yy;
+      const bool exact = !(hh / yy - theta * theta > skip_above);
       double e = 0.0;
       __syncwarp();
 #pragma unroll
@@ -1696,7 +1732,7 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
           y[q] = hy[q] / nz;  // H z_i for the next iteration
           yv[lane + 32 * q] = y[q];
         }
-      const double resid = sqrt(wsum0(e) / yy);
+      const double resid = exact ? sqrt(wsum0(e) / yy) : INFINITY;
       __syncwarp();
       val = theta;
       have = true;
@@ -1707,7 +1743,17 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
     }
     const bool ok = conv || (!broke && have);
     if (lane == 0 && ok && isfinite(val) && fabs(val) > fabs(d->mu)) d->mu = val;  // observe_ritz
+#if PGM_TAIL_TIMING
+    rt1 = gtimer();
+    n_pow = 1;
+#endif
+#if PGM_RITZ_SEQ
+    asm volatile("bar.arrive 2, %0;" ::"n"(RITZ_THREADS));
+#endif
   } else {
+#if PGM_RITZ_SEQ
+    asm volatile("bar.sync 2, %0;" ::"n"(RITZ_THREADS));  // tuning: GJ after the power loop
+#endif
     // ---- meanwhile warps 1..7: H^-1 by Gauss-Jordan with partial pivoting,
     // [H | I] -> [I | H^-1] in smem (named barrier 1 over these 224 threads)
     const int t7 = tid - 32, n7 = RITZ_THREADS - 32;
@@ -1767,6 +1813,9 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
     }
   }
   __syncthreads();
+#if PGM_TAIL_TIMING
+  const unsigned long long rt2 = gtimer();
+#endif
   // ---- smallest_ritz_pair: inverse power iteration (deflation.cpp:31-54),
   // warp 0: y = H^-1 z (smem, lane per row), hy = H y (global); y.y and y.hy
   // in one pass, then the residual while z <- y / |y| is written.
@@ -1797,17 +1846,20 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
       }
       __syncwarp();
       hmv_global(nx, hy);
-      double p = 0.0, qq = 0.0;
+      double p = 0.0, qq = 0.0, hh = 0.0;
 #pragma unroll
       for (int q = 0; q < RQ; ++q)
         if (lane + 32 * q < k) {
           p += y[q] * y[q];
           qq += y[q] * hy[q];
+          hh += hy[q] * hy[q];
         }
-      const double yy = wsum0(p), yhy = wsum0(qq);
+      wsum3(p, qq, hh);
+      const double yy = p, yhy = qq;
       const double nz = sqrt(yy);
       if (!isfinite(nz) || nz == 0.0) break;
       const double theta = yhy / yy;
+      const bool exact = !(hh / yy - theta * theta > skip_above);
       double e = 0.0;
 #pragma unroll
       for (int q = 0; q < RQ; ++q)
@@ -1816,15 +1868,29 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
           e += t * t;
           z[lane + 32 * q] = y[q] / nz;
         }
-      const double resid = sqrt(wsum0(e) / yy);
+      const double resid = exact ? sqrt(wsum0(e) / yy) : INFINITY;
       __syncwarp();
       val = theta;
+#if PGM_TAIL_TIMING
+      ++n_inv;
+#endif
       if (resid <= tol * scale) {
         conv = true;
         break;
       }
     }
   }
+#if PGM_TAIL_TIMING
+  if (lane == 0) {
+    const unsigned long long rt3 = gtimer();
+    atomicAdd(&g_tail_ns[4], rt1 - rt0);   // power iteration (warp 0)
+    atomicAdd(&g_tail_ns[5], rt2 - rt0);   // until Gauss-Jordan done
+    atomicAdd(&g_tail_ns[6], rt3 - rt2);   // inverse iteration
+    atomicAdd(&g_tail_ns[7], (unsigned long long)n_inv);
+    atomicAdd(&g_tail_ns[8], 1ull);
+    (void)n_pow;
+  }
+#endif
   if (conv) {
     for (int l = lane; l < k; l += 32) P.zl[l] = z[l] * P.s[l];
     if (lane == 0) {

@@ -2124,8 +2124,8 @@ pgm_status pgm_deflator_apply(pgm_deflator* d, const double* v, double* w, int32
 // SpMV (ns): [level-1 chain, level 2, finisher, launches]; reset after read
 int pgm_debug_tail(unsigned long long* out) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, g_tail_ns, 4 * sizeof(unsigned long long));
-  unsigned long long z[8] = {};
+  cudaMemcpyFromSymbol(out, g_tail_ns, 9 * sizeof(unsigned long long));
+  unsigned long long z[16] = {};
   cudaMemcpyToSymbol(g_tail_ns, z, sizeof(z));
   return 0;
 }
