@@ -322,6 +322,15 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Wall-clock bound of every cross-rank wait (%globaltimer, ns): generous
+// enough for time-sliced ranks (two processes on one GPU without MPS) and
+// slow starters, yet a protocol fault still ends in PGM_ESTATE, not a hang.
+constexpr unsigned long long PEER_WAIT_NS = 30ull * 1000000000ull;
+__device__ __forceinline__ unsigned long long peer_clock_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 #ifndef PGM_PEER_INLINE
 #define PGM_PEER_INLINE __noinline__
@@ -355,9 +364,10 @@ __device__ PGM_PEER_INLINE void peer_allreduce_impl(double* red, int nv, int W, 
   if (threadIdx.x < W) st_release_sys(peer_flag[threadIdx.x] + par * W + me, e);
   if (threadIdx.x < W) {
     const unsigned long long* f = flag_local + par * W + threadIdx.x;
+    const unsigned long long t_start = peer_clock_ns();
     long long spins = 0;
     while (ld_acquire_sys(f) < e) {
-      if (++spins > (1ll << 24)) {  // ~10 s
+      if ((++spins & 1023) == 0 && peer_clock_ns() - t_start > PEER_WAIT_NS) {
         s_timeout = 1;
         break;
       }

@@ -668,6 +668,134 @@ __global__ void __launch_bounds__(SPMV_THREADS, SPMV_MINB) k_spmv(Sell A, Params
 }
 
 // ---------------------------------------------------------------------------
+// Halo planes over peer memory (world > 1, peer transport: CUDA IPC windows
+// across processes, plain pointers between in-process ranks).  Every rank's
+// window carries two parities x two mailboxes (planes coming from below and
+// from above, hmax doubles each) and their flags.  k_halo_push stores this
+// rank's boundary planes straight into the neighbours' mailboxes (NVLink P2P
+// stores), fences system-wide and — from the last block — raises the
+// neighbours' flags to the exchange epoch; k_halo_pull waits for its own two
+// flags (bounded spin) and copies the mailboxes into the vector's halo rows.
+// Parity reuse is safe: a rank pushes epoch e + 2 only after pulling e + 1,
+// which needs its neighbour's push of e + 1, issued after that neighbour
+// pulled e.  No NCCL, no host synchronisation.
+struct HaloPeerArgs {
+  char* const* win;         // [world] window bases as addressable from this rank
+  char* mine;               // this rank's window
+  size_t off_mb, off_hf;    // byte offsets: mailboxes [2 par][2 dir][hmax], flags [2 par][2 dir]
+  size_t hmax;
+  int me, world;
+  unsigned long long* epoch;  // this rank's halo-exchange counter (in its window)
+  unsigned* cnt;              // push completion counter
+  GState* g;
+};
+
+__device__ __forceinline__ double* halo_mb(char* base, const HaloPeerArgs& A, int par, int dir) {
+  return reinterpret_cast<double*>(base + A.off_mb) + ((size_t)par * 2 + dir) * A.hmax;
+}
+__device__ __forceinline__ unsigned long long* halo_fl(char* base, const HaloPeerArgs& A, int par,
+                                                       int dir) {
+  return reinterpret_cast<unsigned long long*>(base + A.off_hf) + par * 2 + dir;
+}
+
+__global__ void __launch_bounds__(256) k_halo_push(HaloPeerArgs A, const double* own, int n,
+                                                   int dn, int up) {
+  __shared__ int s_last;
+  const unsigned long long e = *A.epoch + 1;
+  const int par = (int)(e & 1ull);
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t t0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (dn > 0) {  // own rows [0, dn) -> below's "from above" mailbox
+    double* dst = halo_mb(A.win[A.me - 1], A, par, 1);
+    for (size_t i = t0; i < (size_t)dn; i += stride) dst[i] = own[i];
+  }
+  if (up > 0) {  // own rows [n - up, n) -> above's "from below" mailbox
+    double* dst = halo_mb(A.win[A.me + 1], A, par, 0);
+    const double* src = own + n - up;
+    for (size_t i = t0; i < (size_t)up; i += stride) dst[i] = src[i];
+  }
+  __threadfence_system();
+  __syncthreads();
+#ifdef PGM_PEER_DEBUG
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    printf("push me %d e %llu dn %d up %d n %d own0 %g ownLast %g\n", A.me, e, dn, up, n, own[0],
+           up > 0 ? own[n - up] : -1.0);
+#endif
+  if (threadIdx.x == 0) s_last = (atomicAdd(A.cnt, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence_system();
+  *A.cnt = 0;
+  *A.epoch = e;
+  if (dn > 0) st_release_sys(halo_fl(A.win[A.me - 1], A, par, 1), e);
+  if (up > 0) st_release_sys(halo_fl(A.win[A.me + 1], A, par, 0), e);
+#ifdef PGM_PEER_DEBUG
+  printf("push me %d raised e %llu at %p / %p\n", A.me, e,
+         dn > 0 ? (void*)halo_fl(A.win[A.me - 1], A, par, 1) : nullptr,
+         up > 0 ? (void*)halo_fl(A.win[A.me + 1], A, par, 0) : nullptr);
+#endif
+}
+
+__global__ void __launch_bounds__(256) k_halo_pull(HaloPeerArgs A, double* vec, int lo, int n,
+                                                   int hi) {
+  __shared__ int s_timeout;
+  const unsigned long long e = *A.epoch;
+  const int par = (int)(e & 1ull);
+  if (threadIdx.x == 0) s_timeout = 0;
+  __syncthreads();
+#ifdef PGM_PEER_DEBUG
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    printf("pull me %d waits e %llu lo %d hi %d at %p / %p\n", A.me, e, lo, hi,
+           (void*)halo_fl(A.mine, A, par, 0), (void*)halo_fl(A.mine, A, par, 1));
+#endif
+  if (threadIdx.x < 2) {
+    const int dir = threadIdx.x;
+    if ((dir == 0 && lo > 0) || (dir == 1 && hi > 0)) {
+      const unsigned long long* f = halo_fl(A.mine, A, par, dir);
+      const unsigned long long t_start = peer_clock_ns();
+      long long spins = 0;
+      while (ld_acquire_sys(f) < e) {
+        if ((++spins & 1023) == 0 && peer_clock_ns() - t_start > PEER_WAIT_NS) {
+          s_timeout = 1;  // a neighbour never pushed
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (s_timeout) {
+    if (threadIdx.x == 0) {
+      A.g->error = 7;  // PGM_ESTATE
+      A.g->active = 0;
+      A.g->done = 1;
+    }
+    return;
+  }
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t t0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const double* from_below = halo_mb(A.mine, A, par, 0);
+#ifdef PGM_PEER_DEBUG
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    printf("pull me %d e %llu lo %d hi %d fb0 %g fa0 %g flags %llu %llu\n", A.me, e, lo, hi,
+           from_below[0], halo_mb(A.mine, A, par, 1)[0], *halo_fl(A.mine, A, par, 0),
+           *halo_fl(A.mine, A, par, 1));
+#endif
+  const double* from_above = halo_mb(A.mine, A, par, 1);
+  for (size_t i = t0; i < (size_t)lo; i += stride) vec[i] = __ldcv(from_below + i);
+  for (size_t i = t0; i < (size_t)hi; i += stride) vec[(size_t)lo + n + i] = __ldcv(from_above + i);
+}
+
+// Newton driver scalars etc. on the peer transport: all-reduce a small device
+// buffer through the same windows and epoch as the reduction kernels.
+__global__ void k_peer_allreduce_buf(Params P, double* buf, int nv) {
+  __shared__ double red[PEER_NV];
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) red[v] = buf[v];
+  __syncthreads();
+  peer_allreduce(red, nv, P);
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) buf[v] = red[v];
+}
+
+// ---------------------------------------------------------------------------
 // x update at the end of a cycle: x += V xc + U cx (gmres.cpp:183-188, with
 // M^{-1} of the correction folded into U cx through the cached U^T V; the
 // coefficients come from k_end_cycle).  Streaming like the DCGS2 update: a

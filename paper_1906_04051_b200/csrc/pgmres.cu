@@ -203,6 +203,7 @@ struct pgm_context {
   // holding the window [2][world][PEER_NV] doubles + flags [2][world] + epoch
   bool peer = false;
   char* pbuf = nullptr;
+  char** d_peer_base = nullptr;  // [world] window bases (char*) for the halo mailboxes
   double** d_peer_win = nullptr;
   unsigned long long** d_peer_flag = nullptr;
   std::vector<void*> peer_opened;  // IPC mappings to close
@@ -700,8 +701,20 @@ Status defl_ensure_hist(pgm_deflator* d, int need) {
 size_t peer_win_bytes(const pgm_context* ctx) {
   return sizeof(double) * 2 * (size_t)ctx->world * PEER_NV;
 }
+// halo mailboxes after the reduction window + flags: [2 par][2 dir][hmax]
+// doubles, then flags [2 par][2 dir], the halo epoch and the push counter
+size_t peer_halo_rows(const pgm_context* ctx) {
+  return std::max<size_t>(std::max(ctx->lo, ctx->hi), 1);
+}
+size_t peer_mb_offset(const pgm_context* ctx) {
+  return round_up(peer_win_bytes(ctx) + sizeof(unsigned long long) * (2 * (size_t)ctx->world + 2),
+                  256);
+}
+size_t peer_hf_offset(const pgm_context* ctx) {
+  return peer_mb_offset(ctx) + sizeof(double) * 4 * peer_halo_rows(ctx);
+}
 size_t peer_buf_bytes(const pgm_context* ctx) {
-  return peer_win_bytes(ctx) + sizeof(unsigned long long) * (2 * (size_t)ctx->world + 2);
+  return peer_hf_offset(ctx) + sizeof(unsigned long long) * 8;
 }
 
 // Peer-pointer tables: wins[q] / flags[q] = rank q's window and flags as
@@ -716,8 +729,10 @@ Status peer_set_tables(pgm_context* ctx, const std::vector<char*>& bufs) {
   }
   if (!ctx->d_peer_win) TRY(dalloc(&ctx->d_peer_win, W));
   if (!ctx->d_peer_flag) TRY(dalloc(&ctx->d_peer_flag, W));
+  if (!ctx->d_peer_base) TRY(dalloc(&ctx->d_peer_base, W));
   CU(cudaMemcpy(ctx->d_peer_win, w.data(), sizeof(double*) * W, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(ctx->d_peer_flag, f.data(), sizeof(void*) * W, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->d_peer_base, bufs.data(), sizeof(char*) * W, cudaMemcpyHostToDevice));
   ctx->peer = true;
   return {};
 }
@@ -1072,6 +1087,8 @@ Status solve_impl(pgm_context* ctx, pgm_matrix* A, pgm_deflator* dflt, const dou
                   const pgm_gmres_config* cfg, int32_t flags, pgm_report* rep) {
   if (!cfg) return einval("pgm_solve: null config");
   if (cfg->m == 0) return einval("GmresWorkspace: m must be positive");
+  if (ctx->world > 1 && !ctx->loop && !ctx->nccl && !ctx->peer)
+    return einval("pgm_solve: a world > 1 context without NCCL needs pgm_peer_import first");
   if (!A || A->ctx != ctx) return einval("pgm_solve: matrix belongs to another context");
   if (A->n != ctx->n) return einval("pgm_solve: matrix rows do not match the partition");
   const bool harvest = dflt != nullptr;
@@ -1458,6 +1475,14 @@ Status matrix_upload(pgm_context* ctx, const pgm_csr_view* a, int32_t flags, pgm
 namespace {
 
 Status allreduce_red(pgm_context* ctx, int nv) {
+  if (ctx->peer) {  // through the peer windows (same epoch sequence as the reduction kernels)
+    if (nv > PEER_NV) return Status{PGM_ESTATE, "allreduce_red: payload exceeds the peer slot"};
+    const Params P = make_params(ctx, ctx->cur_defl ? ctx->cur_defl : ctx->dummy);
+    k_peer_allreduce_buf<<<1, 128, 0, ctx->stream>>>(P, ctx->red_out, nv);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    return {};
+  }
   if (ctx->loop) {
     pgm_loopback* L = ctx->loop;
     CU(cudaStreamSynchronize(ctx->stream));
@@ -1504,6 +1529,28 @@ Status halo_exchange(pgm_context* ctx, HaloKind kind, int slot, cudaStream_t st)
   double* vec = halo_vec(ctx, kind, slot);
   const size_t lo = ctx->lo, hi = ctx->hi, n = ctx->n;
   const int below = ctx->rank - 1, above = ctx->rank + 1;
+  if (ctx->peer) {
+    // boundary planes through the neighbours' peer-memory mailboxes
+    HaloPeerArgs A{};
+    A.win = ctx->d_peer_base;
+    A.mine = ctx->pbuf;
+    A.off_mb = peer_mb_offset(ctx);
+    A.off_hf = peer_hf_offset(ctx);
+    A.hmax = peer_halo_rows(ctx);
+    A.me = ctx->rank;
+    A.world = ctx->world;
+    A.epoch = reinterpret_cast<unsigned long long*>(ctx->pbuf + A.off_hf) + 4;
+    A.cnt = reinterpret_cast<unsigned*>(reinterpret_cast<unsigned long long*>(ctx->pbuf + A.off_hf) + 5);
+    A.g = ctx->g;
+    const int dn = below >= 0 ? (int)lo : 0, up = above < ctx->world ? (int)hi : 0;
+    const int G = std::max(1, std::min(ctx->nsm / 4, (int)((std::max(lo, hi) + 2047) / 2048)));
+    k_halo_push<<<G, 256, 0, st>>>(A, vec + lo, (int)n, dn, up);
+    k_halo_pull<<<G, 256, 0, st>>>(A, vec, below >= 0 ? (int)lo : 0, (int)n,
+                                   above < ctx->world ? (int)hi : 0);
+    ctx->launches += 2;
+    CU(cudaGetLastError());
+    return {};
+  }
   if (ctx->loop) {
     pgm_loopback* L = ctx->loop;
     CU(cudaStreamSynchronize(ctx->stream));
@@ -1702,6 +1749,9 @@ pgm_status pgm_context_create(const pgm_context_config* cfg, pgm_context** out) 
       if ((s = peer_set_tables(ctx, bufs)).code) return bail(s);
     }
     L->barrier();
+  } else if (cfg->world > 1 && !cfg->nccl_id) {
+    // peer-only: no NCCL; halos and reductions go through the CUDA-IPC peer
+    // windows once pgm_peer_import has mapped them (solves refuse before)
   } else if (cfg->world > 1 || cfg->nccl_id) {
     if (!nccl_lite::available()) return bail(Status{PGM_ENCCL, "libnccl.so.2 not loadable"});
     if (!cfg->nccl_id) return bail(Status{PGM_EINVAL, "world > 1 needs an ncclUniqueId"});
@@ -1734,6 +1784,7 @@ void pgm_context_destroy(pgm_context* ctx) {
   ctx->peer_opened.clear();
   dfree(ctx->d_peer_win);
   dfree(ctx->d_peer_flag);
+  dfree(ctx->d_peer_base);
   dfree(ctx->pbuf);
   if (ctx->dummy) pgm_deflator_destroy(ctx->dummy);
   free_workspace(ctx);
@@ -1867,14 +1918,23 @@ pgm_status pgm_spmv(pgm_matrix* a, const double* x, double* y, int32_t flags) {
   pgm_context* ctx = a->ctx;
   cudaSetDevice(ctx->device);
   auto run = [&]() -> Status {
+    TRY(set_gstate_idle(ctx));
+    if (ctx->loop && ctx->peer) {  // in-process peer ranks start the exchange together
+      CU(cudaStreamSynchronize(ctx->stream));
+      ctx->loop->barrier();
+    }
     TRY(copy_in(ctx, ctx->tmp + ctx->lo, x, ctx->n, flags));
     if (ctx->world > 1) TRY(halo_exchange(ctx, HV_TMP));
-    TRY(set_gstate_idle(ctx));
     Params P = make_params(ctx, ctx->dummy);
     PlainEpi E{ctx->tmp, ctx->b + ctx->lo};
     TRY(launch_spmv(ctx, a, P, E, 0));
     TRY(copy_out(ctx, y, ctx->b + ctx->lo, ctx->n, flags));
     CU(cudaStreamSynchronize(ctx->stream));
+    if (ctx->world > 1) {  // a halo wait that timed out flags the state
+      int err = 0;
+      CU(cudaMemcpy(&err, &ctx->g->error, sizeof(int), cudaMemcpyDeviceToHost));
+      if (err) return Status{PGM_ESTATE, "pgm_spmv: a peer rank never delivered its halo planes"};
+    }
     return {};
   };
   Status s = run();

@@ -178,7 +178,8 @@ class DeviceExecutor:
 
     def __init__(self, device: int = 0, *, n_global: int | None = None, n_axis: int = 0,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 loopback: "LoopbackGroup | None" = None, deterministic: bool = False):
+                 loopback: "LoopbackGroup | None" = None, deterministic: bool = False,
+                 peer_only: bool = False):
         """deterministic=True: every reduction is per-plane sequential partials
         + the reference's pairwise fold (parallel.cpp:33-46, 120-131), so the
         solve is bit-identical for any rank count (the reference's
@@ -186,6 +187,9 @@ class DeviceExecutor:
         reductions (bitwise reproducible for a given partition)."""
         self.device, self.rank, self.world = device, rank, world
         self.deterministic = bool(deterministic)
+        # peer_only: world > 1 without NCCL — halos and reductions through the
+        # CUDA-IPC peer windows (peer_export / peer_import before solving)
+        self.peer_only = bool(peer_only)
         self.n_axis = n_axis
         self._nccl_id = nccl_id
         self._loop = loopback
@@ -197,9 +201,10 @@ class DeviceExecutor:
     def _create(self, n_global: int):
         L = capi.lib()
         idbuf = None
-        if self.world > 1 and self._loop is None:
+        if self.world > 1 and self._loop is None and not self.peer_only:
             if self._nccl_id is None or len(self._nccl_id) != 128:
-                raise ValueError("world > 1 needs a 128-byte ncclUniqueId or a LoopbackGroup")
+                raise ValueError("world > 1 needs a 128-byte ncclUniqueId, a LoopbackGroup "
+                                 "or peer_only=True")
         if self._nccl_id is not None and self._loop is None:
             # world = 1 with an id: a 1-rank NCCL communicator (collective mode
             # on one GPU: every reduction goes through ncclAllReduce + k_finish)
