@@ -56,7 +56,9 @@ typedef struct pgm_loopback pgm_loopback;
 typedef struct {
   int32_t device;         /* CUDA ordinal this rank drives                   */
   int32_t rank, world;    /* world = 1: single GPU                           */
-  const void* nccl_id;    /* 128-byte ncclUniqueId from rank 0 (world > 1)   */
+  const void* nccl_id;    /* 128-byte ncclUniqueId from rank 0 (world > 1);  */
+                          /* NULL with world > 1 and no loopback: peer-only  */
+                          /* (no NCCL; solves need pgm_peer_import first)   */
   pgm_loopback* loopback; /* instead of NCCL: in-process group of `world`    */
                           /* contexts driven by one host thread each         */
   uint32_t n_axis;        /* node planes; plane = n_axis^2 rows.  Required   */
@@ -201,9 +203,12 @@ pgm_status pgm_nccl_unique_id(void* out128);
 /* Peer-memory transport (world > 1, one process per GPU): every reduction
  * kernel all-reduces inside its last block by storing its sums into every
  * rank's window over NVLink (CUDA IPC mapping) — no NCCL call, no extra
- * kernel.  Export this rank's 128-byte window handle, gather all ranks'
- * handles in rank order (e.g. torch.distributed.all_gather), import them.
- * Without the import the context keeps the NCCL allreduce.  In-process
+ * kernel — and the halo planes go through mailboxes in the neighbours'
+ * windows (k_halo_push / k_halo_pull).  Export this rank's 128-byte window
+ * handle, gather all ranks' handles in rank order (e.g.
+ * torch.distributed.all_gather), import them.  Without the import an NCCL
+ * context keeps the NCCL allreduce and send/recv halos; a peer-only context
+ * (nccl_id NULL) refuses to solve.  Requires CUDA_MODULE_LOADING=EAGER.  In-process
  * loopback groups use the peer transport by default (PGMRES_PEER=0: off). */
 pgm_status pgm_peer_export(pgm_context* ctx, void* out128);
 pgm_status pgm_peer_import(pgm_context* ctx, const void* all /* world * 128 bytes */);
