@@ -13,7 +13,10 @@ namespace pgm {
 #endif
 constexpr int TILE = PGM_TILE;        // rows per SpMV tile (SELL sort window)
 constexpr int SPT = TILE / 32;        // 32-row slices per tile
-constexpr int SPMV_THREADS = 256;
+#ifndef PGM_SPMV_THREADS
+#define PGM_SPMV_THREADS 256  // threads per SpMV block (one TILE-row tile per block)
+#endif
+constexpr int SPMV_THREADS = PGM_SPMV_THREADS;
 #ifndef PGM_SPMV_UNROLL
 #define PGM_SPMV_UNROLL 4
 #endif
@@ -31,9 +34,6 @@ constexpr int GROUP = 32;             // first-level reduction group (blocks, on
 constexpr int MAX_M = 112;            // Ritz harvest keeps [H | H^-1] in smem
 constexpr int MAX_R1 = 32;            // r_max + 1 bound of the register fast path
 constexpr int RITZ_THREADS = 256;
-#ifndef PGM_RITZ_SEQ
-#define PGM_RITZ_SEQ 0  // tuning: 1 = Gauss-Jordan after (not beside) the power iteration
-#endif
 
 // ---- device state ------------------------------------------------------------
 // Per-solve GMRES control word (gmres.cpp:132-218 loop variables + GmresReport
@@ -180,6 +180,33 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 __shared__ unsigned long long s_tail_t[3];
 #endif
+#ifndef PGM_RED_ACQREL
+#define PGM_RED_ACQREL 1
+#endif
+// Arrival counter of the grid reduction: CTA barrier, then ONE acq_rel RMW by
+// thread 0 (release: the CTA's partials, ordered before it by the barrier;
+// acquire: every earlier arrival's partials) — the pattern of a semaphore
+// arrive, instead of a block-wide __threadfence before and after a relaxed
+// atomic (each fence is a full round trip on the reduction's critical path).
+__device__ __forceinline__ unsigned atom_add_acqrel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+#if PGM_RED_ACQREL
+#define PGM_ARRIVE(ctr, last_at)                                   \
+  __syncthreads();                                                 \
+  if (threadIdx.x == 0) s_flag = (atom_add_acqrel((ctr), 1u) == (unsigned)(last_at)); \
+  __syncthreads();
+#define PGM_ARRIVED_FENCE()
+#else
+#define PGM_ARRIVE(ctr, last_at)                                   \
+  __threadfence();                                                 \
+  __syncthreads();                                                 \
+  if (threadIdx.x == 0) s_flag = (atomicAdd((ctr), 1u) == (unsigned)(last_at)); \
+  __syncthreads();
+#define PGM_ARRIVED_FENCE() __threadfence();
+#endif
 __device__ __forceinline__ bool grid_reduce_ex(const double* bvals, int nv, const Params& P,
                                                double* red, int G, int bid) {
   __shared__ int s_flag;
@@ -189,18 +216,12 @@ __device__ __forceinline__ bool grid_reduce_ex(const double* bvals, int nv, cons
   const int NG = (G + GROUP - 1) / GROUP;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int v = threadIdx.x; v < nv; v += blockDim.x) P.part[(size_t)v * G + bid] = bvals[v];
-  __threadfence();
-  __syncthreads();
   const int grp = bid / GROUP;
   const int g0 = grp * GROUP;
   const int gsize = min(GROUP, G - g0);
-  if (threadIdx.x == 0) {
-    const unsigned t = atomicAdd(&P.cnt[1 + grp], 1u);
-    s_flag = (t == (unsigned)(gsize - 1));
-  }
-  __syncthreads();
+  PGM_ARRIVE(&P.cnt[1 + grp], gsize - 1)
   if (!s_flag) return false;
-  __threadfence();
+  PGM_ARRIVED_FENCE()
   // level 1: lane = block of the group, VPW values per warp pass
   for (int v0 = warp * VPW; v0 < nv; v0 += nw * VPW) {
     double s[VPW];
@@ -218,8 +239,6 @@ __device__ __forceinline__ bool grid_reduce_ex(const double* bvals, int nv, cons
     }
   }
   if (threadIdx.x == 0) P.cnt[1 + grp] = 0;
-  __threadfence();
-  __syncthreads();
   // level 2: with more than GROUP groups, super-groups of GROUP groups are
   // summed by their last group-reducer (distributed), so the final block
   // reads at most GROUP partials per value (a single block walking ~1000
@@ -229,13 +248,9 @@ __device__ __forceinline__ bool grid_reduce_ex(const double* bvals, int nv, cons
   int nlvl = NG;
   if (NS > 1) {
     const int sg = grp / GROUP, s0 = sg * GROUP, ssize = min(GROUP, NG - s0);
-    if (threadIdx.x == 0) {
-      const unsigned t = atomicAdd(&P.cnt[1 + NG + sg], 1u);
-      s_flag = (t == (unsigned)(ssize - 1));
-    }
-    __syncthreads();
+    PGM_ARRIVE(&P.cnt[1 + NG + sg], ssize - 1)
     if (!s_flag) return false;
-    __threadfence();
+    PGM_ARRIVED_FENCE()
     for (int v0 = warp * VPW; v0 < nv; v0 += nw * VPW) {
       double s[VPW];
 #pragma unroll
@@ -252,18 +267,12 @@ __device__ __forceinline__ bool grid_reduce_ex(const double* bvals, int nv, cons
       }
     }
     if (threadIdx.x == 0) P.cnt[1 + NG + sg] = 0;
-    __threadfence();
-    __syncthreads();
     lvl = P.g2part;
     nlvl = NS;
   }
-  if (threadIdx.x == 0) {
-    const unsigned t = atomicAdd(&P.cnt[0], 1u);
-    s_flag = (t == (unsigned)((NS > 1 ? NS : NG) - 1));
-  }
-  __syncthreads();
+  PGM_ARRIVE(&P.cnt[0], (NS > 1 ? NS : NG) - 1)
   if (!s_flag) return false;
-  __threadfence();
+  PGM_ARRIVED_FENCE()
 #if PGM_TAIL_TIMING
   if (threadIdx.x == 0) s_tail_t[1] = gtimer();
 #endif

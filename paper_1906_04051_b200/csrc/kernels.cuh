@@ -1690,6 +1690,133 @@ __device__ __forceinline__ void hmatvec(const double* M, int k, const double* z,
   if (i < k && !half) out[i] = s;
 }
 
+// Row sums of an 8-row x 32-lane tile: a[r] = this lane's partial of row r.
+// Transposing butterfly: lane l ends with the sum over all lanes of row
+// r(l) = 4 b4 + 2 b3 + b2 (b = the bits of l); 9 shuffles for 8 sums, fixed order.
+__device__ __forceinline__ double rowsum8(const double (&a)[8], int lane) {
+  double b[4], c[2];
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    b[q] = (h16 ? a[q + 4] : a[q]) + __shfl_xor_sync(0xffffffffu, h16 ? a[q] : a[q + 4], 16);
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    c[q] = (h8 ? b[q + 2] : b[q]) + __shfl_xor_sync(0xffffffffu, h8 ? b[q] : b[q + 2], 8);
+  double d = (h4 ? c[1] : c[0]) + __shfl_xor_sync(0xffffffffu, h4 ? c[0] : c[1], 4);
+  d += __shfl_xor_sync(0xffffffffu, d, 2);
+  d += __shfl_xor_sync(0xffffffffu, d, 1);
+  return d;
+}
+__device__ __forceinline__ int rowsum8_row(int lane) {
+  return ((lane >> 2) & 1) | (((lane >> 3) & 1) << 1) | (((lane >> 4) & 1) << 2);
+}
+// sum over the 8 row-owner lanes (lane % 4 == 0) of a warp; result in lane 0
+__device__ __forceinline__ double owners_sum(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 16);
+  return v;
+}
+
+// largest_ritz_value (deflation.cpp:57-82) for k <= 64 with the whole CTA:
+// warp w owns rows 8w..8w+7, lane the columns lane and lane + 32, the H
+// entries live in registers (16 per lane); one matvec = 16 FMAs + one
+// transposing butterfly per warp, the three sums y.y, y.Hy, Hy.Hy one smem
+// combine over the 8 warps; two CTA barriers per iteration.  Same iteration
+// as the one-warp version below: y = H z unnormalised, theta = y.Hy / y.y,
+// residual |Hy - theta y| / |y| (exact pass only near convergence).
+__device__ void ritz_power8(const Params& P, int k, int m, double tol, double scale,
+                            double skip_above) {
+  __shared__ double sy[2][64];
+  __shared__ double spart[RITZ_THREADS / 32][4];
+  DState* d = P.d;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t hld = (size_t)m + 1;
+  double h[8][2];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int i = 8 * warp + r, j = lane + 32 * c;
+      h[r][c] = (i < k && j < k && j + 1 >= i) ? __ldcg(P.h_orig + (size_t)j * hld + i) : 0.0;
+    }
+  const int row = 8 * warp + rowsum8_row(lane);
+  const bool owner = (lane & 3) == 0 && row < k;
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) (&sy[0][0])[i] = 0.0;
+  __syncthreads();
+  // y_1 = H z_0, z_0 = 1 / sqrt(k)
+  {
+    const double z0 = 1.0 / sqrt((double)k);
+    double a[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a[r] = h[r][0] * (lane < k ? z0 : 0.0) + h[r][1] * (lane + 32 < k ? z0 : 0.0);
+    const double hy = rowsum8(a, lane);
+    if (owner) sy[0][row] = hy;
+  }
+  __syncthreads();
+  bool have = false, conv = false, broke = false;
+  double val = 0.0;
+  int cur = 0;
+  for (int it = 0; it < d->pow_maxit; ++it) {
+    const double y0 = sy[cur][lane], y1 = sy[cur][lane + 32];
+    double a[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a[r] = h[r][0] * y0 + h[r][1] * y1;
+    const double hy = rowsum8(a, lane);
+    const double yi = owner ? sy[cur][row] : 0.0;
+    double p = owner ? yi * yi : 0.0, q = owner ? yi * hy : 0.0, hh = owner ? hy * hy : 0.0;
+    p = owners_sum(p);
+    q = owners_sum(q);
+    hh = owners_sum(hh);
+    if (lane == 0) {
+      spart[warp][0] = p;
+      spart[warp][1] = q;
+      spart[warp][2] = hh;
+    }
+    __syncthreads();
+    double yy = 0.0, yhy = 0.0, hsq = 0.0;
+#pragma unroll
+    for (int w = 0; w < RITZ_THREADS / 32; ++w) {
+      yy += spart[w][0];
+      yhy += spart[w][1];
+      hsq += spart[w][2];
+    }
+    const double nz = sqrt(yy);
+    if (!isfinite(nz) || nz == 0.0) {
+      broke = true;
+      break;
+    }
+    const double theta = yhy / yy;
+    const bool exact = !(hsq / yy - theta * theta > skip_above);
+    if (owner) sy[cur ^ 1][row] = hy / nz;  // H z_i for the next iteration
+    if (exact) {
+      const double t = hy - theta * yi;
+      const double e = owners_sum(owner ? t * t : 0.0);
+      if (lane == 0) spart[warp][3] = e;
+    }
+    __syncthreads();
+    double resid = INFINITY;
+    if (exact) {
+      double e = 0.0;
+#pragma unroll
+      for (int w = 0; w < RITZ_THREADS / 32; ++w) e += spart[w][3];
+      resid = sqrt(e / yy);
+    }
+    val = theta;
+    have = true;
+#if PGM_TAIL_TIMING
+    if (threadIdx.x == 0) atomicAdd(&g_tail_ns[13], 1ull);
+#endif
+    if (resid <= tol * scale) {
+      conv = true;
+      break;
+    }
+    cur ^= 1;
+  }
+  const bool ok = conv || (!broke && have);
+  if (threadIdx.x == 0 && ok && isfinite(val) && fabs(val) > fabs(d->mu)) d->mu = val;  // observe_ritz
+}
+
 __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
   extern __shared__ double sm[];
   GState* g = P.g;
@@ -1700,9 +1827,12 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
   __shared__ double s_red[32];
   // a new harvest: the previous truncation's rotation has been applied; a
   // rejected push this time must not re-apply it (k_rotate runs regardless)
-  if (tid == 0) d->rotate = 0;
+  // two CTAs: CTA 1 runs the power iteration (running |mu|), CTA 0 the
+  // Gauss-Jordan inverse and the inverse iteration (smallest Ritz pair)
+  const bool main_cta = blockIdx.x == 0;
+  if (tid == 0 && main_cta) d->rotate = 0;
   if (k == 0) {
-    if (tid == 0) {
+    if (tid == 0 && main_cta) {
       d->skipped++;
       d->push_ok = 0;
       d->theta = __longlong_as_double(0x7ff8000000000000LL);
@@ -1736,7 +1866,7 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
   const double scale = sqrt(block_sum(fr, s_red));
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
   if (!(scale > 0.0) || !isfinite(scale)) {
-    if (tid == 0) {
+    if (tid == 0 && main_cta) {
       d->skipped++;
       d->push_ok = 0;
       d->theta = nan;
@@ -1747,7 +1877,6 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
   const int warp = tid >> 5, lane = tid & 31;
 #if PGM_TAIL_TIMING
   const unsigned long long rt0 = gtimer();
-  unsigned long long rt1 = 0;
   int n_pow = 0, n_inv = 0;
 #endif
   // H (Hessenberg block, column-major i + j (m+1)) read by lane-per-row
@@ -1816,7 +1945,17 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
   // formula decides, exactly as deflation.cpp:48-52 / 74-78.
   const double skip_above = fmax(64.0 * 2.220446049250313e-16 * scale * scale,
                                  4.0 * (tol * scale) * (tol * scale));
-  if (warp == 0) {
+  if (!main_cta) {
+#if PGM_TAIL_TIMING
+    const unsigned long long pt0 = gtimer();
+#endif
+    if (k <= 64) ritz_power8(P, k, m, tol, scale, skip_above);
+#if PGM_TAIL_TIMING
+    if (tid == 0) atomicAdd(&g_tail_ns[4], gtimer() - pt0);
+#endif
+    if (k <= 64 || warp != 0) return;
+  }
+  if (!main_cta) {
     // ---- largest_ritz_value: power iteration (deflation.cpp:57-82), one warp,
     // shuffles only.  y = H z_{i-1} unnormalised; theta = y.Hy / y.y = z.Hz;
     // residual |Hy - theta y| / |y| = |Hz - theta z|.
@@ -1832,6 +1971,9 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
     bool have = false, conv = false, broke = false;
     double val = 0.0;
     for (int it = 0; it < d->pow_maxit; ++it) {
+#if PGM_TAIL_TIMING
+      ++n_pow;
+#endif
       hmv_global(yv, hy);
       double p = 0.0, qq = 0.0, hh = 0.0;
 #pragma unroll
@@ -1872,21 +2014,19 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
     const bool ok = conv || (!broke && have);
     if (lane == 0 && ok && isfinite(val) && fabs(val) > fabs(d->mu)) d->mu = val;  // observe_ritz
 #if PGM_TAIL_TIMING
-    rt1 = gtimer();
-    n_pow = 1;
+    if (lane == 0) {
+      atomicAdd(&g_tail_ns[4], gtimer() - rt0);
+      atomicAdd(&g_tail_ns[13], (unsigned long long)n_pow);
+    }
 #endif
-#if PGM_RITZ_SEQ
-    asm volatile("bar.arrive 2, %0;" ::"n"(RITZ_THREADS));
-#endif
-  } else {
-#if PGM_RITZ_SEQ
-    asm volatile("bar.sync 2, %0;" ::"n"(RITZ_THREADS));  // tuning: GJ after the power loop
-#endif
+    return;
+  } else if (warp != 0) {
     // ---- meanwhile warps 1..7: H^-1 by Gauss-Jordan with partial pivoting,
     // [H | I] -> [I | H^-1] in smem (named barrier 1 over these 224 threads)
     const int t7 = tid - 32, n7 = RITZ_THREADS - 32;
     auto gsync = [] { asm volatile("bar.sync 1, %0;" ::"n"(RITZ_THREADS - 32)); };
     for (int e = t7; e < k * k; e += n7) B[e] = ((e % k) == (e / k)) ? 1.0 : 0.0;
+    const int i0 = t7 % k, a0 = t7 / k, di = n7 % k, da = n7 / k;
     gsync();
     for (int c = 0; c < k; ++c) {
       if (warp == 1) {
@@ -1930,12 +2070,26 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
       }
       for (int i = t7; i < k; i += n7) colc[i] = H[i + c * k];
       gsync();
-      for (int e = t7; e < 2 * k * k; e += n7) {
-        const int i = e % k, j = e / k;
-        if (i == c) continue;
-        double* M = j < k ? H : B;
-        const int jj = j < k ? j : j - k;
-        M[i + jj * k] -= colc[i] * M[c + jj * k];
+      // H columns <= c are unit vectors by now (and H itself is not read
+      // after the inverse): only H columns c+1..k-1 and all of B change
+      // (row swaps move B's unit entries, so any B column can have a
+      // nonzero in row c); (row, column) stepped incrementally, no integer
+      // division per element
+      {
+        const int nh = k - 1 - c;
+        int i = i0, a = a0;
+        for (int e = t7; e < k * (nh + k); e += n7) {
+          if (i != c) {
+            double* M = a < nh ? H + (size_t)(c + 1 + a) * k : B + (size_t)(a - nh) * k;
+            M[i] -= colc[i] * M[c];
+          }
+          i += di;
+          a += da;
+          if (i >= k) {
+            i -= k;
+            ++a;
+          }
+        }
       }
       gsync();
     }
@@ -2011,12 +2165,11 @@ __global__ void __launch_bounds__(RITZ_THREADS) k_ritz(Params P, int hcopy) {
 #if PGM_TAIL_TIMING
   if (lane == 0) {
     const unsigned long long rt3 = gtimer();
-    atomicAdd(&g_tail_ns[4], rt1 - rt0);   // power iteration (warp 0)
     atomicAdd(&g_tail_ns[5], rt2 - rt0);   // until Gauss-Jordan done
     atomicAdd(&g_tail_ns[6], rt3 - rt2);   // inverse iteration
     atomicAdd(&g_tail_ns[7], (unsigned long long)n_inv);
     atomicAdd(&g_tail_ns[8], 1ull);
-    (void)n_pow;
+    atomicAdd(&g_tail_ns[13], (unsigned long long)n_pow);
   }
 #endif
   if (conv) {

@@ -1000,7 +1000,8 @@ Status enqueue_cycle(pgm_context* ctx, pgm_matrix* A, pgm_deflator* d, const Par
       CU(cudaFuncSetAttribute(k_ritz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
     {
       ProfScope ps(ctx, PC_RITZ, 0);
-      k_ritz<<<1, RITZ_THREADS, rsmem, ctx->stream>>>(P, hcopy);
+      // CTA 0: Gauss-Jordan + inverse iteration; CTA 1: power iteration
+      k_ritz<<<2, RITZ_THREADS, rsmem, ctx->stream>>>(P, hcopy);
     }
     ctx->launches++;
     CU(cudaGetLastError());
@@ -2181,10 +2182,11 @@ pgm_status pgm_deflator_apply(pgm_deflator* d, const double* v, double* w, int32
 
 #if PGM_TAIL_TIMING
 // tuning variant only: accumulated reduction-tail stamps of the DCGS2 step
-// SpMV (ns): [level-1 chain, level 2, finisher, launches]; reset after read
+// SpMV (ns): [level-1 chain, level 2, finisher, launches, Ritz x5, finisher
+// phases x4]; out must hold 16 values; reset after read
 int pgm_debug_tail(unsigned long long* out) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, g_tail_ns, 9 * sizeof(unsigned long long));
+  cudaMemcpyFromSymbol(out, g_tail_ns, 16 * sizeof(unsigned long long));
   unsigned long long z[16] = {};
   cudaMemcpyToSymbol(g_tail_ns, z, sizeof(z));
   return 0;

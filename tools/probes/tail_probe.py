@@ -17,7 +17,7 @@ A, b = ex.assemble_bratu(ne, 6.8, device=True)
 dA = ex.upload(A)
 x = torch.zeros(ex.n_own, dtype=torch.float64, device="cuda")
 L = _capi.lib()
-buf = (C.c_ulonglong * 4)()
+buf = (C.c_ulonglong * 16)()
 for rep in range(2):
     d = pg.Deflator(pg.DeflationConfig(), ex)
     x.zero_()
@@ -27,4 +27,5 @@ for rep in range(2):
     nl = max(1, buf[3])
     print(f"n_e={ne} solve {r.solve_seconds*1e3:.1f} ms, {r.total_inner} steps; per step SpMV: "
           f"level1 {buf[0]/nl/1e3:.2f} us, level2 {buf[1]/nl/1e3:.2f} us, finisher "
-          f"{buf[2]/nl/1e3:.2f} us over {buf[3]} launches")
+          f"{buf[2]/nl/1e3:.2f} us over {buf[3]} launches; finisher phases (loads, serial, "
+          f"coefficients, tail) " + " ".join(f"{buf[9 + q]/nl/1e3:.2f}" for q in range(4)) + " us")
