@@ -1084,6 +1084,48 @@ Status copy_out(pgm_context* ctx, double* dst, const double* src_own, size_t n, 
   return {};
 }
 
+#ifndef PGM_L2WIN
+#define PGM_L2WIN 1
+#endif
+// L2 persistence for the small dense solver state the finishers and the SpMV
+// prologues chase every step (Hessenberg, rotations, scales, coefficients,
+// U^T V, T^-1, the status words): written by one step's finisher and read by
+// the next, they would otherwise be evicted by the basis / matrix streams in
+// between (18 GB per step at config 3).  One access-policy window over the
+// span of these allocations when it is compact (<= 4 MB).
+void set_l2_window(pgm_context* ctx, pgm_deflator* d) {
+  if (!PGM_L2WIN) return;
+  if (const char* e = std::getenv("PGMRES_L2WIN"))
+    if (e[0] == '0') return;
+  const size_t m = (size_t)ctx->ws_m, R1 = (size_t)std::max(d->R1, 1);
+  const std::pair<const void*, size_t> r[] = {
+      {ctx->s, 8 * (m + 2)},          {ctx->h_orig, 8 * (m + 1) * m}, {ctx->h_rot, 8 * (m + 1) * m},
+      {ctx->gv, 8 * (m + 2)},         {ctx->cs, 8 * (m + 1)},         {ctx->sn, 8 * (m + 1)},
+      {ctx->coefA, 8 * (m + 2)},      {ctx->coefB, 8 * (m + 2)},      {ctx->tU, 8 * (m + 2) * R1},
+      {ctx->c, 8 * (R1 + 1)},         {ctx->g, sizeof(GState)},       {d->d, sizeof(DState)},
+      {d->Tinv, 8 * R1 * R1},         {ctx->cnt, 64}};
+  uintptr_t lo = UINTPTR_MAX, hi = 0;
+  for (const auto& e : r) {
+    if (!e.first) continue;
+    lo = std::min(lo, (uintptr_t)e.first);
+    hi = std::max(hi, (uintptr_t)e.first + e.second);
+  }
+  if (hi <= lo || hi - lo > ((size_t)4 << 20)) return;
+  static bool limit = false;
+  if (!limit) {
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)4 << 20);
+    limit = true;
+  }
+  cudaStreamAttrValue v{};
+  v.accessPolicyWindow.base_ptr = (void*)lo;
+  v.accessPolicyWindow.num_bytes = hi - lo;
+  v.accessPolicyWindow.hitRatio = 1.0f;
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+  cudaGetLastError();  // best effort
+}
+
 Status solve_impl(pgm_context* ctx, pgm_matrix* A, pgm_deflator* dflt, const double* b, double* x,
                   const pgm_gmres_config* cfg, int32_t flags, pgm_report* rep) {
   if (!cfg) return einval("pgm_solve: null config");
@@ -1111,6 +1153,7 @@ Status solve_impl(pgm_context* ctx, pgm_matrix* A, pgm_deflator* dflt, const dou
   ctx->dc_now = ctx->dcgs2 && !(ctx->peer && 2 * m + 2 + d->R1 > PEER_NV);
   TRY(ensure_workspace(ctx, m, maxr, std::max(d->R1, 1)));
   TRY(defl_alloc_vectors(d));
+  set_l2_window(ctx, d);
   if (harvest) {
     DState hs;
     CU(cudaMemcpy(&hs, d->d, sizeof(DState), cudaMemcpyDeviceToHost));
