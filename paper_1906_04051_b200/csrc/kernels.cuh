@@ -1384,7 +1384,10 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_cgs2_update(Params P, int k) {
 // DCGS2 update pass (one stream over W_0..W_{k-1}, u_k = W_k, y = W_{k+1}):
 //   q_k (unnormalised)  W_k     = u + sum_{l<k} coefA_l W_l          (k >= 1)
 //   u_{k+1}             W_{k+1} = coefA_k y + sum_{l<k} coefB_l W_l + coefB_k W_k'
-__global__ void __launch_bounds__(UPD_BLOCK) k_dcgs2_update(Params P, int k) {
+#ifndef PGM_UPD_MINB
+#define PGM_UPD_MINB 1  // min resident blocks per SM (register cap) of the DCGS2 update pass
+#endif
+__global__ void __launch_bounds__(UPD_BLOCK, PGM_UPD_MINB) k_dcgs2_update(Params P, int k) {
   __shared__ double ca[MAX_M + 32], cb[MAX_M + 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = P.n;
